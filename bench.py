@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the G4 ring-accumulation hot path (BASELINE.json metric:
+"G4 updates/sec & HBM GB/s per GPU at 1/2/4/8 B200; max G4 size; vs CPU ref").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B] [--dtype c128|c64]
+    torchrun --nproc-per-node N bench.py --gpus N ...          (N > 1: the ring)
+    python bench.py --impl reference ...                      (CPU reference arm)
+
+Workload (BASELINE config 2): Nc=16 x 32 frequencies -> N = 512 combined
+indices; exchange planes K3 in [0, 64) (16 momenta x 4 frequencies under
+K = w*n_k + k); complex128; synthetic payloads from the reference's
+counter-based generator (run on the device).  One "step" = one measurement
+round: every rank contributes B walkers, the walkers travel the S-rank ring
+(S = N GPUs), and every rank applies all S*B walkers to its 64/S planes.
+At N=1 a step is one K1 pass of B walkers over the 64-plane slice (268 MB,
+larger than L2, so no flush is needed between steps).
+
+value  = G4 updates/s of the whole job (payloads resident in HBM).
+e2e    = the same through the reference-facing C ABI (g4_accumulate) with
+         payloads in pinned HOST memory in reference layout: H2D copy +
+         stage (K2) + update (K1) + D2H of a probe row of the slice per step.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+CONFIGS = {
+    # name: (n_k, n_w, planes, description)
+    "c1": (4, 8, 1, "Nc=4 (2x2), 8 freqs, K3={0}"),
+    "c2": (16, 32, 64, "Nc=16 (4x4), 32 freqs, 16 k x 4 w exchange planes"),
+    "c3": (16, 64, 64, "Nc=16, 64 freqs, 64 exchange planes"),
+    "c4": (36, 128, 576, "Nc=36 (6x6), 128 freqs, 36 k x 16 w exchange planes"),
+}
+
+
+def measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            d = json.loads(p.read_text())
+            return float(d["hbm_gbs"]), "measured"
+        except Exception:
+            pass
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled DURING the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except (OSError, FileNotFoundError):
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 9:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[5 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side (reference arm and cpu_baseline): the numpy port of accumulate_g4
+# (oracle/oracle.py, "kind": "port") in one process per host core, each on a
+# disjoint K3 range (make_partition), same payloads -- BASELINE.md section 2.
+
+def _cpu_worker(conn, n, lo, hi, walkers, seed):
+    import numpy as np
+    from oracle import oracle as O
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    gs = [O.gsigma(seed, 0, w, 0, n, "float") for w in range(walkers)]
+    g4 = np.zeros((hi - lo, n, n), np.complex128)
+    while True:
+        msg = conn.recv()
+        if msg is None:
+            break
+        t0 = time.perf_counter()
+        for up, down in gs[:msg]:
+            O.accumulate_np(g4, lo, hi, up, down)
+        conn.send(time.perf_counter() - t0)
+
+
+class CpuPool:
+    def __init__(self, n, planes, walkers, cores, seed=0):
+        import multiprocessing as mp
+        from oracle import oracle as O
+        ctx = mp.get_context("fork")
+        self.cores = max(1, min(cores, planes))
+        self.ranges = O.partition(planes, self.cores)
+        self.conns, self.procs = [], []
+        for lo, hi in self.ranges:
+            a, b = ctx.Pipe()
+            p = ctx.Process(target=_cpu_worker, args=(b, n, lo, hi, walkers, seed), daemon=True)
+            p.start()
+            self.conns.append(a)
+            self.procs.append(p)
+
+    def step(self, walkers):
+        t0 = time.perf_counter()
+        for c in self.conns:
+            c.send(walkers)
+        worker_t = [c.recv() for c in self.conns]
+        return time.perf_counter() - t0, max(worker_t)
+
+    def close(self):
+        for c in self.conns:
+            c.send(None)
+        for p in self.procs:
+            p.join(timeout=10)
+
+
+def cpu_throughput(n, planes, walkers, steps, warmup, cores):
+    pool = CpuPool(n, planes, walkers, cores)
+    try:
+        for _ in range(warmup):
+            pool.step(walkers)
+        times = [pool.step(walkers)[0] for _ in range(steps)]
+    finally:
+        pool.close()
+    upd = planes * n * n * walkers
+    return upd / statistics.mean(times), statistics.mean(times), pool.cores
+
+
+def cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def run_reference(args):
+    """--impl reference: the reference algorithm on the host cores (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    n_k, n_w, planes, desc = CONFIGS[args.config]
+    n = n_k * n_w
+    cores = O.cpu_count()
+    walkers = args.batch
+    rate, step_s, used = cpu_throughput(n, planes, walkers, args.steps, args.warmup, cores)
+    line = {
+        "metric": "G4 updates/s", "value": rate, "unit": "updates/s", "impl": "reference",
+        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
+        "data": "synthetic (reference generator, float mode, seed 0)",
+        "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
+                   "walkers_per_step": walkers},
+        "cpu_baseline": {"value": rate, "unit": "updates/s", "cores": used, "kind": "port",
+                         "sample": f"{walkers} walkers x {planes} planes x N^2={n * n} per step, "
+                                   f"numpy port of accumulate_g4 in {used} processes on disjoint "
+                                   f"K3 ranges; host {cpu_model()}"},
+        "e2e": {"value": rate, "unit": "updates/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+
+def run_gpu(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2105_00027_b200 import _lib
+    from paper_2105_00027_b200 import tensor as T
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+        from paper_2105_00027_b200 import engine  # noqa: F401  (ring path, see run_ring)
+        return run_ring(args)
+
+    lib = _lib.load()
+    n_k, n_w, planes, desc = CONFIGS[args.config]
+    sp = T.CombinedIndexSpace(n_k, n_w)
+    n = sp.size
+    dtype = torch.complex128 if args.dtype == "c128" else torch.complex64
+    eb = 16 if args.dtype == "c128" else 8
+    B = args.batch
+    sl = T.GtSlice.zeros(sp, 0, planes, device=dev, dtype=dtype)
+    pools = [[T.GSigma.empty(sp, device=dev, dtype=dtype) for _ in range(B)] for _ in range(2)]
+    for i, pool in enumerate(pools):
+        T.fill_gsigmas(pool, 0, [T.Origin(0, 0, w, i, 0) for w in range(B)], "float")
+    stream = torch.cuda.current_stream(dev)
+
+    def step(i):
+        T.accumulate_g4_batch(sl, pools[i % 2])
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.steps)]
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        time.sleep(0.3)  # let the sampler start
+        torch.cuda.synchronize()
+        t_start.record(stream)
+        for i in range(args.steps):
+            ev[i][0].record(stream)
+            step(i)
+            ev[i][1].record(stream)
+        t_end.record(stream)
+        torch.cuda.synchronize()
+    total_ms = t_start.elapsed_time(t_end)
+    k_ms = [a.elapsed_time(b) for a, b in ev]
+    upd_step = B * planes * n * n
+    value = upd_step * args.steps / (total_ms * 1e-3)
+    peak, peak_kind = measured_peaks()
+    alg_bytes = 2 * planes * n * n * eb + B * 2 * n * n * eb
+    achieved = alg_bytes / (statistics.mean(k_ms) * 1e-3) / 1e9
+
+    # -- e2e: reference-layout payloads in pinned host memory through g4_accumulate --
+    e2e = run_e2e(args, lib, T, sp, planes, dtype, eb, dev)
+
+    line = {
+        "metric": "G4 updates/s", "value": value, "unit": "updates/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "data": "synthetic (reference counter-based generator on device, float mode, seed 0)",
+        "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
+                   "walkers_per_pass": B, "subring_size": 1, "lanes": 1,
+                   "l2": "slice larger than L2 (no flush needed)" if planes * n * n * eb > 126e6
+                   else "slice fits L2 (L2-resident caveat)"},
+        "hbm_gbs": achieved,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": None,
+                     "peak_source": peak_kind, "kernel": "k_accumulate",
+                     "bytes_per_launch": alg_bytes},
+        "clocks": clk.summary(),
+        "e2e": e2e,
+        "gpu_launches": args.steps,
+        "g4_bytes": sl.nbytes,
+    }
+    if not args.no_cpu_baseline:
+        from oracle import oracle as O
+        cores = O.cpu_count()
+        rate, step_s, used = cpu_throughput(n, planes, B, max(2, args.cpu_steps), 1, cores)
+        line["cpu_baseline"] = {
+            "value": rate, "unit": "updates/s", "cores": used, "kind": "port",
+            "sample": f"{max(2, args.cpu_steps)} steps of {B} walkers x {planes} planes x N^2={n * n}, "
+                      f"numpy port of accumulate_g4 in {used} processes on disjoint K3 ranges; "
+                      f"host {cpu_model()}"}
+    print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, lib, T, sp, planes, dtype, eb, dev):
+    import torch
+    n = sp.size
+    B = args.batch
+    code = _dtype_code(dtype)
+    sl = T.GtSlice.zeros(sp, 0, planes, device=dev, dtype=dtype)
+    host = []
+    for i in range(2):
+        ups, downs = [], []
+        for w in range(B):
+            u, d = T.generate_reference_layout(0, T.Origin(0, 0, w, i, 0), sp, "float", device=dev,
+                                               dtype=dtype)
+            ups.append(u.cpu().pin_memory())
+            downs.append(d.cpu().pin_memory())
+        host.append((ups, downs))
+    dev_bufs = [([torch.empty((n, n), dtype=dtype, device=dev) for _ in range(B)],
+                 [torch.empty((n, n), dtype=dtype, device=dev) for _ in range(B)]) for _ in range(2)]
+    ws_bytes = lib.g4_accumulate_workspace_bytes(n, B, code)
+    ws = torch.empty(ws_bytes, dtype=torch.uint8, device=dev)
+    probe = torch.empty(n, dtype=dtype).pin_memory()
+    comp = torch.cuda.current_stream(dev)
+    copy = torch.cuda.Stream(dev)
+    from paper_2105_00027_b200 import _lib
+    ready = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+
+    def h2d(i):
+        j = i % 2
+        with torch.cuda.stream(copy):
+            copy.wait_event(done[j])
+            for w in range(B):
+                dev_bufs[j][0][w].copy_(host[j][0][w], non_blocking=True)
+                dev_bufs[j][1][w].copy_(host[j][1][w], non_blocking=True)
+            ready[j].record(copy)
+
+    def compute(i):
+        j = i % 2
+        comp.wait_event(ready[j])
+        _lib.check(lib.g4_accumulate(
+            sl.data.data_ptr(), 0, planes, n, _lib.ptr_array([t.data_ptr() for t in dev_bufs[j][0]]),
+            _lib.ptr_array([t.data_ptr() for t in dev_bufs[j][1]]), B, code, 0, ws.data_ptr(),
+            ws_bytes, comp.cuda_stream), "g4_accumulate")
+        done[j].record(comp)
+        probe.copy_(sl.data[0, 0], non_blocking=True)
+
+    for j in range(2):
+        done[j].record(comp)
+    steps, warm = args.steps, args.warmup
+    h2d(0)
+    for i in range(warm):
+        if i + 1 < warm + steps:
+            h2d(i + 1)
+        compute(i)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record(comp)
+    for i in range(warm, warm + steps):
+        if i + 1 < warm + steps:
+            h2d(i + 1)
+        compute(i)
+    t1.record(comp)
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    # the H2D of the first timed step was issued before t0; account it explicitly
+    return {"value": B * planes * n * n * steps / (ms * 1e-3), "unit": "updates/s",
+            "h2d_bytes_per_step": B * 2 * n * n * eb, "d2h_bytes_per_step": n * eb,
+            "path": "g4_accumulate (C ABI, reference layout) from pinned host buffers; "
+                    "H2D double-buffered on a copy stream; D2H probe row per step"}
+
+
+def _dtype_code(dtype):
+    import torch
+    return 0 if dtype == torch.complex128 else 1
+
+
+def run_ring(args):  # filled in by the ring engine (paper_2105_00027_b200.engine)
+    from paper_2105_00027_b200.bench_ring import run_ring_bench
+    return run_ring_bench(args)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--batch", type=int, default=8, help="walkers per K1 pass (per rank)")
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
+    ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gpu(args)
+
+
+if __name__ == "__main__":
+    main()

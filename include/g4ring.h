@@ -1,0 +1,150 @@
+/*
+ * g4ring.h -- C ABI of the B200-native G4 ring-accumulation library (libg4ring.so).
+ *
+ * Drop-in boundary for the hot path of the reference package `ringacc`
+ * (/root/reference/pkg/src/ringacc).  Every entry point names the reference
+ * interface it replaces.  Conventions:
+ *   - extern "C", plain pointers and sizes, no C++ or torch types;
+ *   - all device pointers are BORROWED for the duration of the stream-ordered
+ *     operation; the caller owns the memory (torch tensors in the Python layer);
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream);
+ *   - every function returns a g4_status; on failure g4_last_error() returns a
+ *     thread-local message.  Status codes map 1:1 onto the reference exception
+ *     hierarchy (ringacc/errors.py:8-27).
+ *
+ * Data layouts (ringacc/tensor.py):
+ *   - G4 slice: data[k3 - lo][k1][k2], C-contiguous complex (re, im interleaved),
+ *     K3 outermost -- GtSlice.data (tensor.py:99-136), bit-for-bit.
+ *   - Walker payload, reference layout: up[N][N] then down[N][N] complex
+ *     (GSigma.up / .down, tensor.py:77-96; wire body order wire.py:32-33).
+ *   - Walker payload, staged layout (device-internal, produced by
+ *     g4_prepare_g / g4_generate, consumed by g4_accumulate_staged, and the form
+ *     that travels around the ring): stg[r][c] = { up[c][r], down[c][r] }, i.e.
+ *     the transposes of both spins interleaved per element (32 B per element
+ *     for complex128, 16 B for complex64).  Same byte count as the reference
+ *     payload body.
+ */
+#ifndef G4RING_H
+#define G4RING_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define G4RING_ABI_VERSION 1
+#define G4_MAX_BATCH 64 /* walkers per accumulate launch (more are chunked) */
+
+typedef enum {
+    G4_OK = 0,
+    G4_ERR_CONTRACT = 1,  /* ringacc.errors.ContractViolation */
+    G4_ERR_CONFIG = 2,    /* ringacc.errors.ConfigError       */
+    G4_ERR_TRANSPORT = 3, /* ringacc.errors.TransportError    */
+    G4_ERR_DEADLOCK = 4,  /* ringacc.errors.DeadlockError     */
+    G4_ERR_CUDA = 5       /* CUDA runtime/driver failure      */
+} g4_status;
+
+typedef enum {
+    G4_C128 = 0, /* complex128: ENTRY_BYTES = 16 (tensor.py:23) -- the reference dtype */
+    G4_C64 = 1   /* complex64: the paper's production G_sigma precision; 1e-5 tolerance */
+} g4_dtype;
+
+typedef enum {
+    G4_MODE_FLOAT = 0,  /* VALUE_MODES[0]: unit-disk complex values (tensor.py:199-203) */
+    G4_MODE_INTEGER = 1 /* VALUE_MODES[1]: Gaussian-integer lattice {-2..2} (tensor.py:204-209) */
+} g4_value_mode;
+
+typedef enum {
+    /* The only update rule the reference implements (tensor.py:233-251,
+     * PAPER.md Eq. 1):  G4[K3][K1][K2] += sum_sigma G_sigma(K3-K2, K3-K1) G_-sigma(K2, K1). */
+    G4_CHANNEL_EQ1 = 0
+} g4_channel;
+
+/* Last error message of the calling thread ("" if none). */
+const char* g4_last_error(void);
+/* G4RING_ABI_VERSION of the loaded library. */
+int32_t g4_abi_version(void);
+/* Bytes of one walker payload in staged (== reference) layout: 2 * n * n * entry bytes.
+ * Replaces GSigma.nbytes (tensor.py:86-89) / wire body length (wire.py:23-24). */
+int64_t g4_payload_bytes(int32_t n, int32_t dtype);
+
+/* Cyclic K difference (a - b) mod n; replaces index_diff (tensor.py:50-55).
+ * Out-of-range a or b -> G4_ERR_CONTRACT. */
+g4_status g4_index_diff(int64_t a, int64_t b, int64_t n, int64_t* out);
+
+/* Balanced contiguous K3 partition over p ranks, remainder to the lowest ranks;
+ * replaces make_partition (tensor.py:148-164).  ranges: 2*p int64 (lo, hi). */
+g4_status g4_make_partition(int64_t n, int64_t p, int64_t* ranges);
+
+/* K2: reference layout -> staged layout for `nbatch` walkers.  up[i], down[i] are
+ * N x N complex (dtype_in); staged[i] receives the staged payload (dtype_out).
+ * Supported (dtype_in, dtype_out): (C128, C128), (C64, C64), (C128, C64). */
+g4_status g4_prepare_g(void* const* staged, const void* const* up, const void* const* down,
+                       int32_t nbatch, int32_t n, int32_t dtype_in, int32_t dtype_out,
+                       void* stream);
+
+/* K3: device-side deterministic payload generator; replaces fill_gsigma /
+ * generate_gsigma (tensor.py:215-228) with the same SplitMix64 key scheme,
+ * keyed on (seed, world_rank, lane, meas) per walker i.  Any of staged / up /
+ * down may be NULL (staged: staged layout; up/down: reference layout).
+ * Integer mode is bitwise equal to the reference; float mode within 2 ulp. */
+g4_status g4_generate(void* const* staged, void* const* up, void* const* down,
+                      int32_t nbatch, uint64_t seed, const int64_t* world_rank,
+                      const int64_t* lane, const int64_t* meas, int32_t n, int32_t mode,
+                      int32_t dtype, void* stream);
+
+/* K1: the G4 slice update; replaces accumulate_g4 (tensor.py:233-251) for a
+ * batch of walkers applied in order 0..nbatch-1 (bitwise identical to nbatch
+ * sequential reference calls).  g4: slice for planes [lo, hi) of an N-point
+ * index space; staged[i]: staged payloads (g4 dtype).  Planes outside [lo, hi)
+ * are never touched.  0 <= lo < hi <= n else G4_ERR_CONTRACT (tensor.py:112-115). */
+g4_status g4_accumulate_staged(void* g4, int64_t lo, int64_t hi, int32_t n,
+                               const void* const* staged, int32_t nbatch, int32_t dtype,
+                               int32_t channel, void* stream);
+
+/* Convenience form taking reference-layout payloads: prepares each batch into
+ * `workspace` (>= g4_accumulate_workspace_bytes) then calls g4_accumulate_staged. */
+int64_t g4_accumulate_workspace_bytes(int32_t n, int32_t nbatch, int32_t dtype);
+g4_status g4_accumulate(void* g4, int64_t lo, int64_t hi, int32_t n, const void* const* up,
+                        const void* const* down, int32_t nbatch, int32_t dtype,
+                        int32_t channel, void* workspace, int64_t workspace_bytes,
+                        void* stream);
+
+/* ---- ring transport over CUDA peer memory (replaces the Communicator plugin's
+ * isend/irecv payload path, ringacc/transport/base.py:53-80, for device
+ * buffers).  Buffers are exported once with CUDA IPC; every ring step is a
+ * copy-engine peer copy plus a 64-bit sequence flag written into the
+ * receiver's memory (no SM cycles, no host round trip). ----------------------- */
+
+#define G4_IPC_HANDLE_BYTES 64
+
+/* Export / import a device allocation between processes (cudaIpc*MemHandle). */
+g4_status g4_ipc_export(void* dev_ptr, void* handle_out /* G4_IPC_HANDLE_BYTES */);
+g4_status g4_ipc_import(const void* handle, void** dev_ptr_out);
+g4_status g4_ipc_close(void* dev_ptr);
+
+/* Stream-ordered peer copy (copy engine over NVLink/NVSwitch, or local). */
+g4_status g4_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+
+/* Stream-ordered 64-bit flag write / wait (cuStreamWriteValue64 /
+ * cuStreamWaitValue64 with GEQ).  `flag` may be a peer (IPC-mapped) address. */
+g4_status g4_flag_write(void* flag, uint64_t value, void* stream);
+g4_status g4_flag_wait(const void* flag, uint64_t value, void* stream);
+/* Host-side poll of a device flag with timeout (deadlock detection,
+ * replaces the recv timeout -> DeadlockError of inprocess.py:54-60).
+ * Returns G4_ERR_DEADLOCK if *flag < value after timeout_ms. */
+g4_status g4_flag_host_wait(const void* flag, uint64_t value, int64_t timeout_ms);
+
+/* Canonical-order slice reduction over peer memory; replaces
+ * Communicator.reduce_sum (transport/base.py:126-149): dst = src[0] + src[1] + ...
+ * summed left to right per entry (rank order), count complex entries.
+ * src[i] may be peer addresses; dst may alias src[0]. */
+g4_status g4_reduce_sum(void* dst, const void* const* src, int32_t nsrc, int64_t count,
+                        int32_t dtype, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* G4RING_H */

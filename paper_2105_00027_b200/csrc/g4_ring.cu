@@ -1,0 +1,178 @@
+// g4_ring.cu -- device plumbing of the ring driver: CUDA IPC export/import of
+// ring buffers, copy-engine peer copies, stream-ordered 64-bit sequence flags,
+// and the canonical-order slice reduction over peer memory.
+//
+// Replaces the payload path of the reference's Communicator plugin
+// (ringacc/transport/base.py:53-80: isend/irecv/PendingOp.wait) and its
+// reduce_sum collective (base.py:126-149) for device-resident buffers.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <thread>
+
+#include <cuda.h>
+
+#include "g4_common.cuh"
+#include "g4_internal.h"
+
+namespace g4 {
+
+// cuStreamWriteValue64 / cuStreamWaitValue64 fetched at run time through the
+// runtime's driver entry point, so libg4ring.so has no link-time libcuda dep.
+using PFN_write64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using PFN_wait64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+
+static g4_status driver_fn(const char* name, void** fn) {
+    cudaDriverEntryPointQueryResult q{};
+    cudaError_t e = cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !*fn) {
+        set_error("driver entry point %s unavailable (%s)", name, cudaGetErrorString(e));
+        return G4_ERR_CUDA;
+    }
+    return G4_OK;
+}
+
+template <typename R>
+struct RedParams {
+    Cx<R>* dst;
+    const Cx<R>* src[G4_MAX_BATCH];
+    int32_t nsrc;
+    int64_t count;
+};
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ RedParams<R> P) {
+    Cx<R>* dst = P.dst;
+    const auto& src = P.src;
+    const int nsrc = P.nsrc;
+    const int64_t count = P.count;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        Cx<R> t = src[0][i];
+        for (int s = 1; s < nsrc; ++s) {  // canonical rank order 0, 1, 2, ...
+            const Cx<R> v = src[s][i];
+            t.re = add_rn(t.re, v.re);
+            t.im = add_rn(t.im, v.im);
+        }
+        dst[i] = t;
+    }
+}
+
+}  // namespace g4
+
+extern "C" {
+
+g4_status g4_ipc_export(void* dev_ptr, void* handle_out) {
+    using namespace g4;
+    if (!dev_ptr || !handle_out) return fail(G4_ERR_CONTRACT, "ipc_export: null pointer");
+    static_assert(sizeof(cudaIpcMemHandle_t) == G4_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    G4_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+    std::memcpy(handle_out, &h, sizeof(h));
+    return G4_OK;
+}
+
+g4_status g4_ipc_import(const void* handle, void** dev_ptr_out) {
+    using namespace g4;
+    if (!handle || !dev_ptr_out) return fail(G4_ERR_CONTRACT, "ipc_import: null pointer");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof(h));
+    G4_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return G4_OK;
+}
+
+g4_status g4_ipc_close(void* dev_ptr) {
+    using namespace g4;
+    if (!dev_ptr) return G4_OK;
+    G4_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    return G4_OK;
+}
+
+g4_status g4_copy_async(void* dst, const void* src, int64_t bytes, void* stream) {
+    using namespace g4;
+    if (bytes < 0 || ((!dst || !src) && bytes > 0)) return fail(G4_ERR_CONTRACT, "copy_async: bad args");
+    if (bytes == 0) return G4_OK;
+    G4_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                            static_cast<cudaStream_t>(stream)));
+    return G4_OK;
+}
+
+g4_status g4_flag_write(void* flag, uint64_t value, void* stream) {
+    using namespace g4;
+    static PFN_write64 fn = nullptr;
+    if (!flag || !aligned(flag, 8)) return fail(G4_ERR_CONTRACT, "flag_write: bad flag pointer");
+    if (!fn) G4_TRY(driver_fn("cuStreamWriteValue64", reinterpret_cast<void**>(&fn)));
+    CUresult r = fn(static_cast<CUstream>(stream), (CUdeviceptr)flag, (cuuint64_t)value,
+                    CU_STREAM_WRITE_VALUE_DEFAULT);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuStreamWriteValue64 failed (CUresult %d)", (int)r);
+        return G4_ERR_TRANSPORT;
+    }
+    return G4_OK;
+}
+
+g4_status g4_flag_wait(const void* flag, uint64_t value, void* stream) {
+    using namespace g4;
+    static PFN_wait64 fn = nullptr;
+    if (!flag || !aligned(flag, 8)) return fail(G4_ERR_CONTRACT, "flag_wait: bad flag pointer");
+    if (!fn) G4_TRY(driver_fn("cuStreamWaitValue64", reinterpret_cast<void**>(&fn)));
+    CUresult r = fn(static_cast<CUstream>(stream), (CUdeviceptr)flag, (cuuint64_t)value,
+                    CU_STREAM_WAIT_VALUE_GEQ);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuStreamWaitValue64 failed (CUresult %d)", (int)r);
+        return G4_ERR_TRANSPORT;
+    }
+    return G4_OK;
+}
+
+g4_status g4_flag_host_wait(const void* flag, uint64_t value, int64_t timeout_ms) {
+    using namespace g4;
+    if (!flag || !aligned(flag, 8)) return fail(G4_ERR_CONTRACT, "flag_host_wait: bad flag pointer");
+    const auto t0 = std::chrono::steady_clock::now();
+    uint64_t cur = 0;
+    for (;;) {
+        G4_CUDA(cudaMemcpy(&cur, flag, sizeof(cur), cudaMemcpyDeviceToHost));
+        if (cur >= value) return G4_OK;
+        const auto ms = std::chrono::duration_cast<std::chrono::milliseconds>(
+                            std::chrono::steady_clock::now() - t0).count();
+        if (ms >= timeout_ms) {
+            set_error("flag wait timed out after %lld ms (have %llu, want %llu)", (long long)ms,
+                      (unsigned long long)cur, (unsigned long long)value);
+            return G4_ERR_DEADLOCK;
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(200));
+    }
+}
+
+g4_status g4_reduce_sum(void* dst, const void* const* src, int32_t nsrc, int64_t count, int32_t dtype,
+                        void* stream) {
+    using namespace g4;
+    if (nsrc < 1 || nsrc > G4_MAX_BATCH || count < 0 || !dst || !src)
+        return fail(G4_ERR_CONTRACT, "reduce_sum: bad args");
+    if (count == 0) return G4_OK;
+    auto st = static_cast<cudaStream_t>(stream);
+    for (int i = 0; i < nsrc; ++i)
+        if (!src[i]) return fail(G4_ERR_CONTRACT, "reduce_sum: null source");
+    const unsigned blocks = (unsigned)std::min<int64_t>((count + 255) / 256, 148 * 16);
+    if (dtype == G4_C128) {
+        RedParams<double> p{};
+        p.dst = static_cast<Cx<double>*>(dst);
+        for (int i = 0; i < nsrc; ++i) p.src[i] = static_cast<const Cx<double>*>(src[i]);
+        p.nsrc = nsrc;
+        p.count = count;
+        k_reduce<double><<<blocks, 256, 0, st>>>(p);
+    } else if (dtype == G4_C64) {
+        RedParams<float> p{};
+        p.dst = static_cast<Cx<float>*>(dst);
+        for (int i = 0; i < nsrc; ++i) p.src[i] = static_cast<const Cx<float>*>(src[i]);
+        p.nsrc = nsrc;
+        p.count = count;
+        k_reduce<float><<<blocks, 256, 0, st>>>(p);
+    } else {
+        return fail(G4_ERR_CONTRACT, "reduce_sum: unknown dtype");
+    }
+    G4_CUDA(cudaGetLastError());
+    return G4_OK;
+}
+
+}  // extern "C"

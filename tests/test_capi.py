@@ -1,0 +1,89 @@
+"""The C-ABI library: builds, loads without a GPU, exports every symbol that
+include/g4ring.h declares, and its host-only entry points match the reference.
+No compute calls (CPU-only container)."""
+import ctypes
+import json
+import re
+
+import pytest
+
+from paper_2105_00027_b200 import _lib
+from paper_2105_00027_b200 import errors
+from paper_2105_00027_b200 import tensor as T
+
+from .conftest import GOLDEN, ROOT
+
+
+def header_symbols():
+    text = (ROOT / "include" / "g4ring.h").read_text()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(g4_[a-z0-9_]+)\s*\(", text)))
+
+
+def test_library_exports_every_header_symbol():
+    lib = _lib.load(build_if_missing=True)
+    syms = header_symbols()
+    assert len(syms) >= 18
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_lib.SIGNATURES), "ctypes table out of sync with include/g4ring.h"
+    assert lib.g4_abi_version() == _lib.ABI_VERSION
+
+
+def test_payload_bytes():
+    lib = _lib.load()
+    assert lib.g4_payload_bytes(512, _lib.G4_C128) == 2 * 512 * 512 * 16
+    assert lib.g4_payload_bytes(4608, _lib.G4_C64) == 2 * 4608 * 4608 * 8
+    assert lib.g4_payload_bytes(0, _lib.G4_C128) == -1
+
+
+def test_index_diff_known_answers():
+    misc = json.loads((GOLDEN / "misc.json").read_text())
+    for a, b, n, want in misc["index_diff"]:
+        # any (n_k, n_w) factorisation; the reference works on the combined index
+        assert T.index_diff(a, b, T.CombinedIndexSpace(1, n)) == want
+    sp = T.CombinedIndexSpace(2, 2)
+    for a, b in ((4, 0), (0, -1)):
+        with pytest.raises(errors.ContractViolation):
+            T.index_diff(a, b, sp)
+
+
+def test_partition_known_answers():
+    misc = json.loads((GOLDEN / "misc.json").read_text())
+    for n, p, ranges in misc["partition"]:
+        assert [list(r) for r in T.make_partition(n, p).ranges] == ranges
+    with pytest.raises(errors.ContractViolation):
+        T.make_partition(4, 5)
+    with pytest.raises(errors.ContractViolation):
+        T.make_partition(4, 0)
+
+
+@pytest.mark.parametrize("n,p", [(1, 1), (7, 3), (64, 64), (4608, 8), (576, 7)])
+def test_partition_invariants(n, p):
+    r = T.make_partition(n, p).ranges
+    sizes = [hi - lo for lo, hi in r]
+    assert r[0][0] == 0 and r[-1][1] == n and max(sizes) - min(sizes) <= 1
+    assert all(a[1] == b[0] for a, b in zip(r, r[1:]))
+
+
+def test_index_space_rejects_bad_dims():
+    with pytest.raises(errors.ContractViolation):
+        T.CombinedIndexSpace(0, 3)
+    sp = T.CombinedIndexSpace(16, 32)
+    assert sp.size == 512 and sp.combined(3, 2) == 35
+
+
+def test_no_cpu_fallback():
+    """Slices and payloads refuse host tensors instead of computing on CPU."""
+    import torch
+    sp = T.CombinedIndexSpace(2, 2)
+    with pytest.raises(errors.ContractViolation):
+        T.GtSlice(sp, 0, 4, torch.zeros((4, 4, 4), dtype=torch.complex128))
+
+
+def test_status_mapping():
+    lib = _lib.load()
+    out = ctypes.c_int64()
+    st = lib.g4_index_diff(9, 0, 4, ctypes.byref(out))
+    with pytest.raises(errors.ContractViolation, match="out of range"):
+        _lib.check(st)

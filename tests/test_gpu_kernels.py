@@ -1,0 +1,275 @@
+"""Parity of the CUDA kernels (called through the C ABI via the mirror API)
+against the CPU oracle and the reference's golden vectors.  GPU only.
+
+Tolerances: complex128 results are BITWISE equal to the oracle (the kernel
+uses the reference's exact op order); complex64 results are bitwise equal to
+the binary32 oracle and within 1e-5 relative of the complex128 reference
+(north_star); float-mode payloads generated ON THE DEVICE differ from numpy's
+by <= 2 ulp (device sin/cos), so those comparisons use atol 1e-15 per entry.
+"""
+import numpy as np
+import pytest
+import torch
+
+from paper_2105_00027_b200 import _lib
+from paper_2105_00027_b200 import tensor as T
+from paper_2105_00027_b200.errors import ContractViolation
+
+pytestmark = pytest.mark.gpu
+
+
+def to_np(t):
+    torch.cuda.synchronize()
+    return t.detach().cpu().numpy()
+
+
+def payload(up, down, dev, dtype=torch.complex128):
+    n = up.shape[0]
+    return T.GSigma(T.CombinedIndexSpace(1, n), up, down, device=dev, dtype=dtype)
+
+
+def test_accumulate_matches_reference_golden(golden, cuda_dev):
+    a = golden("acc.npz")
+    for i in range(len([k for k in a.files if k.endswith("_meta")])):
+        nk, nw, lo, hi, nwalk = (int(x) for x in a[f"c{i}_meta"])
+        sp = T.CombinedIndexSpace(nk, nw)
+        sl = T.GtSlice(sp, lo, hi, torch.from_numpy(a[f"c{i}_start"]).to(cuda_dev))
+        gs = [T.GSigma(sp, a[f"c{i}_up"][w], a[f"c{i}_down"][w], device=cuda_dev) for w in range(nwalk)]
+        for g in gs:
+            T.accumulate_g4(sl, g)
+        assert np.array_equal(to_np(sl.data), a[f"c{i}_end"]), f"case {i}"
+        assert sl.meas_count == int(a[f"c{i}_count"])
+        # the batched form is bitwise identical to sequential calls
+        sl2 = T.GtSlice(sp, lo, hi, torch.from_numpy(a[f"c{i}_start"]).to(cuda_dev))
+        T.accumulate_g4_batch(sl2, gs)
+        assert torch.equal(sl.data, sl2.data)
+
+
+@pytest.mark.parametrize("n,lo,hi,nb", [(64, 0, 64, 1), (64, 13, 29, 3), (96, 90, 96, 5),
+                                        (33, 0, 33, 17), (128, 64, 72, 70), (5, 1, 4, 2),
+                                        (1, 0, 1, 3), (2, 0, 2, 4), (3, 2, 3, 9)])
+def test_random_shapes_bitwise_vs_oracle(oracle, cuda_dev, n, lo, hi, nb):
+    rng = np.random.default_rng(n * 1000 + lo)
+    start = rng.standard_normal((hi - lo, n, n)) + 1j * rng.standard_normal((hi - lo, n, n))
+    ref = start.copy()
+    sp = T.CombinedIndexSpace(1, n)
+    sl = T.GtSlice(sp, lo, hi, torch.from_numpy(start).to(cuda_dev))
+    gs = []
+    for _ in range(nb):
+        up = rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n))
+        down = rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n))
+        oracle.accumulate(ref, lo, hi, up, down)
+        gs.append(T.GSigma(sp, up, down, device=cuda_dev))
+    T.accumulate_g4_batch(sl, gs)  # > G4_MAX_BATCH walkers are chunked in order
+    assert np.array_equal(to_np(sl.data), ref)
+
+
+def test_config1_device_generator(golden, cuda_dev):
+    """BASELINE config 1: N=32, K3={0}, 16 walkers generated on the device."""
+    c1 = golden("c1.npz")
+    sp = T.CombinedIndexSpace(4, 8)
+    for key in c1.files:
+        mode, seed = key.split("_")
+        sl = T.GtSlice.zeros(sp, 0, 1, device=cuda_dev)
+        gs = [T.generate_gsigma(int(seed), T.Origin(0, 0, w, 0, 0), sp, mode, device=cuda_dev)
+              for w in range(16)]
+        T.accumulate_g4_batch(sl, gs)
+        got = to_np(sl.data)
+        if mode == "integer":
+            assert np.array_equal(got, c1[key])
+        else:
+            np.testing.assert_allclose(got, c1[key], rtol=1e-10, atol=1e-13)
+        assert sl.meas_count == 16
+
+
+@pytest.mark.parametrize("mode", ["integer", "float"])
+def test_generator_vs_oracle(oracle, cuda_dev, mode):
+    for (seed, wr, lane, meas, nk, nw) in [(0, 0, 0, 0, 2, 2), (1234, 9, 3, 4, 4, 8),
+                                           (2**40 + 3, 7, 5, 999, 3, 5), (11, 1, 0, 2, 16, 32)]:
+        sp = T.CombinedIndexSpace(nk, nw)
+        ref_up, ref_down = oracle.gsigma(seed, wr, lane, meas, sp.size, mode)
+        g = T.generate_gsigma(seed, T.Origin(0, 0, lane, meas, wr), sp, mode, device=cuda_dev)
+        up, down = to_np(g.up), to_np(g.down)
+        ru, rd = T.generate_reference_layout(seed, T.Origin(0, 0, lane, meas, wr), sp, mode,
+                                             device=cuda_dev)
+        if mode == "integer":
+            assert np.array_equal(up, ref_up) and np.array_equal(down, ref_down)
+            assert np.array_equal(to_np(ru), ref_up) and np.array_equal(to_np(rd), ref_down)
+        else:
+            for x, y in ((up, ref_up), (down, ref_down), (to_np(ru), ref_up), (to_np(rd), ref_down)):
+                np.testing.assert_allclose(x, y, rtol=0, atol=1e-15)
+
+
+def test_prepare_is_exact_transpose(cuda_dev):
+    rng = np.random.default_rng(1)
+    for n in (1, 7, 32, 33, 100):
+        up = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        down = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+        g = payload(up, down, cuda_dev)
+        st = to_np(g.staged)
+        assert np.array_equal(st[:, :, 0], up.T) and np.array_equal(st[:, :, 1], down.T)
+        assert np.array_equal(to_np(g.up.contiguous()), up)
+
+
+def test_identity_known_answer(cuda_dev):
+    """Both spins = I: every plane gains 2 on its K1 == K2 diagonal."""
+    for n in (2, 5, 40):
+        sp = T.CombinedIndexSpace(1, n)
+        eye = np.eye(n, dtype=np.complex128)
+        sl = T.GtSlice.zeros_full(sp, device=cuda_dev)
+        T.accumulate_g4(sl, T.GSigma(sp, eye, eye, device=cuda_dev))
+        expected = np.zeros((n, n, n), np.complex128)
+        for k3 in range(n):
+            expected[k3][np.diag_indices(n)] = 2
+        assert np.array_equal(to_np(sl.data), expected)
+
+
+def test_zero_payload_only_bumps_count(cuda_dev):
+    sp = T.CombinedIndexSpace(2, 2)
+    sl = T.GtSlice.zeros_full(sp, device=cuda_dev)
+    T.accumulate_g4(sl, T.GSigma.empty(sp, device=cuda_dev))
+    assert int(torch.count_nonzero(sl.data)) == 0 and sl.meas_count == 1
+
+
+def test_guard_planes_never_written(cuda_dev):
+    sp = T.CombinedIndexSpace(2, 3)
+    n = sp.size
+    backing = torch.full((n, n, n), 99 + 99j, dtype=torch.complex128, device=cuda_dev)
+    sl = T.GtSlice(sp, 2, 4, backing[2:4])
+    T.accumulate_g4(sl, T.generate_gsigma(9, T.Origin(0, 0, 0, 0, 0), sp, device=cuda_dev))
+    b = to_np(backing)
+    for plane in (0, 1, 4, 5):
+        assert np.all(b[plane] == 99 + 99j)
+    assert not np.all(b[2] == 99 + 99j)
+
+
+def test_guard_planes_large(cuda_dev):
+    """Same at a kernel-relevant size: 4 owned planes inside 12, N=160."""
+    sp = T.CombinedIndexSpace(16, 10)
+    n = sp.size
+    backing = torch.full((12, n, n), -7 + 3j, dtype=torch.complex128, device=cuda_dev)
+    sl = T.GtSlice(sp, 5, 9, backing[4:8])
+    gs = [T.generate_gsigma(3, T.Origin(0, 0, w, 0, 0), sp, device=cuda_dev) for w in range(5)]
+    T.accumulate_g4_batch(sl, gs)
+    b = to_np(backing)
+    assert np.all(b[:4] == -7 + 3j) and np.all(b[8:] == -7 + 3j)
+
+
+@pytest.mark.parametrize("n,p", [(6, 4), (12, 5), (64, 8)])
+def test_slice_sum_equivalence(cuda_dev, n, p):
+    """Per-slice accumulation over a partition stitches to the full tensor, bitwise."""
+    sp = T.CombinedIndexSpace(1, n)
+    gs = [T.generate_gsigma(17, T.Origin(0, 0, 0, m, 0), sp, "integer", device=cuda_dev) for m in range(3)]
+    full = T.GtSlice.zeros_full(sp, device=cuda_dev)
+    T.accumulate_g4_batch(full, gs)
+    stitched = torch.zeros_like(full.data)
+    for lo, hi in T.make_partition(n, p).ranges:
+        sl = T.GtSlice.zeros(sp, lo, hi, device=cuda_dev)
+        for g in gs:
+            T.accumulate_g4(sl, g)
+        stitched[lo:hi] = sl.data
+    assert torch.equal(stitched, full.data)
+
+
+def test_order_independent_in_integer_mode(cuda_dev):
+    sp = T.CombinedIndexSpace(4, 4)
+    a = T.generate_gsigma(1, T.Origin(0, 0, 0, 0, 0), sp, "integer", device=cuda_dev)
+    b = T.generate_gsigma(1, T.Origin(0, 1, 0, 0, 1), sp, "integer", device=cuda_dev)
+    ab, ba = T.GtSlice.zeros_full(sp, device=cuda_dev), T.GtSlice.zeros_full(sp, device=cuda_dev)
+    T.accumulate_g4_batch(ab, [a, b])
+    T.accumulate_g4_batch(ba, [b, a])
+    assert torch.equal(ab.data, ba.data)
+
+
+def test_contract_violations(cuda_dev):
+    sp = T.CombinedIndexSpace(2, 2)
+    g = T.generate_gsigma(0, T.Origin(0, 0, 0, 0, 0), sp, device=cuda_dev)
+    with pytest.raises(ContractViolation):
+        T.accumulate_g4(T.GtSlice.zeros_full(T.CombinedIndexSpace(2, 3), device=cuda_dev), g)
+    with pytest.raises(ContractViolation):
+        T.GtSlice.zeros(sp, 3, 3, device=cuda_dev)
+    with pytest.raises(ContractViolation):
+        T.accumulate_g4(T.GtSlice.zeros_full(sp, device=cuda_dev, dtype=torch.complex64), g)
+    lib = _lib.load()
+    sl = T.GtSlice.zeros_full(sp, device=cuda_dev)
+    st = lib.g4_accumulate_staged(sl.data.data_ptr(), 0, 4, 4, _lib.ptr_array([g.staged.data_ptr()]),
+                                  1, _lib.G4_C128, 7, None)
+    with pytest.raises(ContractViolation, match="channel"):
+        _lib.check(st)
+    st = lib.g4_accumulate_staged(sl.data.data_ptr() + 8, 0, 4, 4,
+                                  _lib.ptr_array([g.staged.data_ptr()]), 1, _lib.G4_C128, 0, None)
+    with pytest.raises(ContractViolation, match="aligned"):
+        _lib.check(st)
+
+
+def test_complex64(oracle, cuda_dev):
+    rng = np.random.default_rng(8)
+    n, lo, hi = 48, 10, 18
+    sp = T.CombinedIndexSpace(1, n)
+    ref128 = np.zeros((hi - lo, n, n), np.complex128)
+    ref64 = np.zeros((hi - lo, n, n), np.complex64)
+    sl = T.GtSlice.zeros(sp, lo, hi, device=cuda_dev, dtype=torch.complex64)
+    gs = []
+    for _ in range(6):
+        up = (rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n))).astype(np.complex64)
+        down = (rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n))).astype(np.complex64)
+        oracle.accumulate(ref128, lo, hi, up.astype(np.complex128), down.astype(np.complex128))
+        oracle.accumulate(ref64, lo, hi, up, down)
+        gs.append(T.GSigma(sp, up, down, device=cuda_dev, dtype=torch.complex64))
+    T.accumulate_g4_batch(sl, gs)
+    got = to_np(sl.data)
+    assert np.array_equal(got, ref64)
+    np.testing.assert_allclose(got, ref128, rtol=1e-5, atol=1e-5 * np.abs(ref128).max())
+
+
+def test_c128_payload_staged_as_c64(cuda_dev):
+    rng = np.random.default_rng(2)
+    n = 20
+    up = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    down = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    g = payload(up, down, cuda_dev, dtype=torch.complex64)
+    assert np.array_equal(to_np(g.staged)[:, :, 0], up.T.astype(np.complex64))
+
+
+def test_reduce_sum_canonical_order(cuda_dev):
+    lib = _lib.load()
+    rng = np.random.default_rng(4)
+    srcs = [rng.standard_normal((3, 17, 17)) + 1j * rng.standard_normal((3, 17, 17)) for _ in range(5)]
+    ts = [torch.from_numpy(s).to(cuda_dev) for s in srcs]
+    dst = torch.empty_like(ts[0])
+    _lib.check(lib.g4_reduce_sum(dst.data_ptr(), _lib.ptr_array([t.data_ptr() for t in ts]), 5,
+                                 ts[0].numel(), _lib.G4_C128,
+                                 torch.cuda.current_stream().cuda_stream))
+    total = srcs[0].copy()
+    for s in srcs[1:]:
+        total += s  # base.py:135-148: rank order 0, 1, 2, ...
+    assert np.array_equal(to_np(dst), total)
+
+
+def test_flag_write_wait_single_process(cuda_dev):
+    lib = _lib.load()
+    flag = torch.zeros(2, dtype=torch.int64, device=cuda_dev)
+    s = torch.cuda.current_stream().cuda_stream
+    _lib.check(lib.g4_flag_write(flag.data_ptr(), 5, s))
+    _lib.check(lib.g4_flag_wait(flag.data_ptr(), 5, s))
+    torch.cuda.synchronize()
+    assert int(flag[0]) == 5
+    _lib.check(lib.g4_flag_host_wait(flag.data_ptr(), 5, 1000))
+    with pytest.raises(Exception) as e:
+        _lib.check(lib.g4_flag_host_wait(flag.data_ptr(), 6, 50))
+    assert type(e.value).__name__ == "DeadlockError"
+
+
+@pytest.mark.parametrize("n,planes", [(512, (0, 1, 63)), (4608, (0, 575))])
+def test_full_size_sampled_planes(oracle, cuda_dev, n, planes):
+    """BASELINE C2 / C4 index space sizes: sampled planes vs the C oracle, bitwise."""
+    sp = T.CombinedIndexSpace(16 if n == 512 else 36, 32 if n == 512 else 128)
+    gs = [T.generate_gsigma(0, T.Origin(0, 0, w, 0, 0), sp, "float", device=cuda_dev) for w in range(2)]
+    host = [(to_np(g.up.contiguous()), to_np(g.down.contiguous())) for g in gs]
+    for q in planes:
+        sl = T.GtSlice.zeros(sp, q, q + 1, device=cuda_dev)
+        T.accumulate_g4_batch(sl, gs)
+        ref = np.zeros((1, n, n), np.complex128)
+        for up, down in host:
+            oracle.accumulate(ref, q, q + 1, up, down)
+        assert np.array_equal(to_np(sl.data), ref), f"plane {q}"
