@@ -19,10 +19,12 @@
  *     (GSigma.up / .down, tensor.py:77-96; wire body order wire.py:32-33).
  *   - Walker payload, staged layout (device-internal, produced by
  *     g4_prepare_g / g4_generate, consumed by g4_accumulate_staged, and the form
- *     that travels around the ring): stg[r][c] = { up[c][r], down[c][r] }, i.e.
- *     the transposes of both spins interleaved per element (32 B per element
- *     for complex128, 16 B for complex64).  Same byte count as the reference
- *     payload body.
+ *     that travels around the ring): spin-planar transposes with a cyclic halo,
+ *       stg[s][r][c] = M_s[c mod N][r mod N],   s = 0 (up), 1 (down),
+ *       0 <= r < N + G4_HALO_ROWS,  0 <= c < LD = N + G4_HALO_COLS  (row pitch LD).
+ *     The core stg[s][0:N][0:N] is the transpose of the reference matrix; the
+ *     halo replicates it cyclically so that every window the update kernel
+ *     fetches (TMA boxes along rows and along the K3-diagonal) is contiguous.
  */
 #ifndef G4RING_H
 #define G4RING_H
@@ -36,6 +38,8 @@ extern "C" {
 
 #define G4RING_ABI_VERSION 1
 #define G4_MAX_BATCH 64 /* walkers per accumulate launch (more are chunked) */
+#define G4_HALO_ROWS 32 /* staged-layout halo (see above) */
+#define G4_HALO_COLS 64
 
 typedef enum {
     G4_OK = 0,
@@ -66,9 +70,12 @@ typedef enum {
 const char* g4_last_error(void);
 /* G4RING_ABI_VERSION of the loaded library. */
 int32_t g4_abi_version(void);
-/* Bytes of one walker payload in staged (== reference) layout: 2 * n * n * entry bytes.
- * Replaces GSigma.nbytes (tensor.py:86-89) / wire body length (wire.py:23-24). */
+/* Bytes of one walker payload in the staged device layout:
+ * 2 * (n + G4_HALO_ROWS) * (n + G4_HALO_COLS) * entry bytes (the reference's
+ * GSigma.nbytes, tensor.py:86-89, is the 2 * n * n core of it). */
 int64_t g4_payload_bytes(int32_t n, int32_t dtype);
+/* Staged-layout geometry: rows per spin plane and row pitch (elements). */
+g4_status g4_staged_dims(int32_t n, int32_t* rows, int32_t* ld);
 
 /* Cyclic K difference (a - b) mod n; replaces index_diff (tensor.py:50-55).
  * Out-of-range a or b -> G4_ERR_CONTRACT. */
@@ -103,6 +110,12 @@ g4_status g4_generate(void* const* staged, void* const* up, void* const* down,
 g4_status g4_accumulate_staged(void* g4, int64_t lo, int64_t hi, int32_t n,
                                const void* const* staged, int32_t nbatch, int32_t dtype,
                                int32_t channel, void* stream);
+
+/* Select the K1 implementation (process-wide): 0 = v1 (register-blocked,
+ * L1-shared direct loads; the default), 1 = v2 (TMA-bulk staged through a
+ * shared-memory ring, warp-specialised; used for N >= 64).  For A/B
+ * measurement and parity tests of both paths (env G4RING_KERNEL). */
+g4_status g4_set_kernel_variant(int32_t variant);
 
 /* Convenience form taking reference-layout payloads: prepares each batch into
  * `workspace` (>= g4_accumulate_workspace_bytes) then calls g4_accumulate_staged. */

@@ -21,6 +21,7 @@ G4_MODE_FLOAT, G4_MODE_INTEGER = 0, 1
 G4_CHANNEL_EQ1 = 0
 G4_MAX_BATCH = 64
 G4_IPC_HANDLE_BYTES = 64
+G4_HALO_ROWS, G4_HALO_COLS = 32, 64
 ABI_VERSION = 1
 
 # (name, restype, argtypes) for every symbol include/g4ring.h declares.
@@ -31,11 +32,13 @@ SIGNATURES = {
     "g4_last_error": (ctypes.c_char_p, []),
     "g4_abi_version": (_i32, []),
     "g4_payload_bytes": (_i64, [_i32, _i32]),
+    "g4_staged_dims": (_i32, [_i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "g4_index_diff": (_i32, [_i64, _i64, _i64, _i64p]),
     "g4_make_partition": (_i32, [_i64, _i64, _i64p]),
     "g4_prepare_g": (_i32, [_vpp, _vpp, _vpp, _i32, _i32, _i32, _i32, _vp]),
     "g4_generate": (_i32, [_vpp, _vpp, _vpp, _i32, _u64, _i64p, _i64p, _i64p, _i32, _i32, _i32, _vp]),
     "g4_accumulate_staged": (_i32, [_vp, _i64, _i64, _i32, _vpp, _i32, _i32, _i32, _vp]),
+    "g4_set_kernel_variant": (_i32, [_i32]),
     "g4_accumulate_workspace_bytes": (_i64, [_i32, _i32, _i32]),
     "g4_accumulate": (_i32, [_vp, _i64, _i64, _i32, _vpp, _vpp, _i32, _i32, _i32, _vp, _i64, _vp]),
     "g4_ipc_export": (_i32, [_vp, _vp]),

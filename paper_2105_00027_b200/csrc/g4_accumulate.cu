@@ -3,31 +3,56 @@
 // Reference semantics, per owned plane K3 = q and entry (k1, k2):
 //   G4[q][k1][k2] += up[(q-k2)%N][(q-k1)%N] * down[k2][k1]
 //                  + down[(q-k2)%N][(q-k1)%N] * up[k2][k1]
-// On the staged payload stg[r][c] = {up[c][r], down[c][r]} this reads
-//   S = stg[(q-k1)%N][(q-k2)%N]   ("shifted")   and   D = stg[k1][k2]   ("direct"):
+// On the staged payload (g4_common.cuh: stg[0][r][c] = up[c][r],
+// stg[1][r][c] = down[c][r], rows of pitch LD with a cyclic halo) this reads
+//   S = stg[.][(q-k1)%N][(q-k2)%N]   ("shifted")  and  D = stg[.][k1][k2]  ("direct"):
 //   p1 = S.u * D.d ; p2 = S.d * D.u ; t = p1 + p2 ; G += t
-// which is the reference's exact op order (tensor.py:250: u*down + d*up, then +=).
+// -- the reference's exact op order (tensor.py:250: u*down + d*up, then +=).
 //
-// Work decomposition (HBM-bound gather-multiply-accumulate; no tensor cores):
-//   * one thread owns a PP x DD block of G4 entries: planes q0..q0+PP-1 and the
-//     diagonal (k1_0 + d, c + d), d < DD.  For such a block the shifted index
-//     (q-k1, q-k2) depends only on m = p - d, so PP*DD updates per walker need
-//     only DD direct and PP+DD-1 shifted staged loads (one 256-bit load each for
-//     complex128: both spins of one element);
-//   * a warp's 32 lanes own 32 consecutive k2 columns: every G4 access is a
-//     contiguous 512 B row segment (coalesced 128-bit loads/stores), every
-//     staged access a contiguous 1 KB row segment (forward or reversed);
-//   * the G4 block is read once, receives all `nbatch` walkers in order
-//     (bitwise equal to nbatch sequential reference calls), written once:
-//     HBM traffic per pass = 2 * P * N^2 * eb + staged reads;
-//   * blockIdx.x = plane chunk (fastest) so concurrently resident CTAs share
-//     the same (k1, k2) tile and its staged rows stay in L2.
+// Register block (both kernels): one thread owns PP x DD = 4 x 4 G4 entries:
+// planes q0..q0+3 x the diagonal (k1_0 + d, c + d), d < 4.  The shifted index
+// (q-k1, q-k2) then depends only on m = p - d, so the 16 updates of one walker
+// need 4 direct + 7 shifted staged elements.  A warp's 32 lanes own 32
+// consecutive k2 columns: G4 rows are read/written as contiguous 512 B runs,
+// staged rows as contiguous (forward or reversed) runs.  The G4 block is read
+// once, receives every walker of the batch in order (bitwise identical to
+// sequential reference calls), and is written once: HBM traffic per pass is
+// 2 * P * N^2 * 16 B plus the staged payloads.
+//
+// v1 (k_accumulate): CTA = WARPS warps stacked along K3 (they share the direct
+//    elements and most shifted rows through L1); loads straight from global.
+// v2 (k_accumulate_tma, complex128, N >= 64): warp-specialised.  One producer
+//    lane streams, per walker, two TMA tensor boxes into a 4-stage shared-memory
+//    ring: the CTA's direct tile (4 rows x 35 cols x 2 spins) through a plain
+//    tensor map, and its whole shifted band (19 diagonal row segments x 32
+//    cols x 2 spins) through a *sheared* tensor map (row stride LD+1 elements)
+//    that turns the diagonal band into a rectangular box.  The halo of the
+//    staged layout means no box ever wraps.  Consumers (4 warps, planes
+//    q0..q0+15) wait on the stage's mbarrier, read their elements from shared
+//    memory (contiguous per warp: conflict-free) and release the stage.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <unordered_map>
+
+#include <cuda.h>
 
 #include "g4_common.cuh"
 #include "g4_internal.h"
 
 namespace g4 {
+
+// Kernel selection: 0 = auto (v2 for complex128 with N >= 64, else v1),
+// 1 = v1 everywhere, 2 = v2 wherever it applies.  G4RING_KERNEL overrides.
+static int g_variant = -1;
+static int kernel_variant() {
+    if (g_variant < 0) {
+        const char* e = getenv("G4RING_KERNEL");
+        g_variant = e ? atoi(e) : 0;
+    }
+    return g_variant;
+}
 
 template <typename R>
 struct AccParams {
@@ -35,7 +60,7 @@ struct AccParams {
     int64_t lo, hi;
     int32_t n;
     int32_t nbatch;
-    const Stg<R>* stg[G4_MAX_BATCH];
+    const Cx<R>* stg[G4_MAX_BATCH];  // staged payloads (2 x ROWS x LD)
 };
 
 __device__ __forceinline__ int wrap(int x, int n) {
@@ -44,31 +69,31 @@ __device__ __forceinline__ int wrap(int x, int n) {
     return x;
 }
 
-template <typename R, int PP, int DD, int WARPS>
-__global__ void __launch_bounds__(32 * WARPS)
+// ---------------------------------------------------------------------------
+// v1
+template <typename R, int PP, int DD, int WARPS, int MINB>
+__global__ void __launch_bounds__(32 * WARPS, MINB)
 k_accumulate(const __grid_constant__ AccParams<R> P) {
     constexpr int NS = PP + DD - 1;  // distinct shifted elements per thread
     const int n = P.n;
-    const int k1_0 = (blockIdx.z * WARPS + threadIdx.y) * DD;
-    if (k1_0 >= n) return;  // warp-uniform
+    const int ld = staged_ld(n);
+    const int64_t plane_s = staged_plane(n);
+    const int k1_0 = blockIdx.z * DD;
     const int c_raw = blockIdx.y * 32 + threadIdx.x;
     const bool col_ok = c_raw < n;
     const int c = col_ok ? c_raw : 0;
-    const int64_t q0 = P.lo + (int64_t)blockIdx.x * PP;
+    const int64_t q0 = P.lo + ((int64_t)blockIdx.x * WARPS + threadIdx.y) * PP;
+    if (q0 >= P.hi) return;  // warp-uniform
 
-    // Direct operand offsets: stg[k1_0 + d][(c + d) % N].
-    int offd[DD];
-    int colg[DD];
-    bool rowok[DD];
+    // Direct elements stg[k1_0 + d][(c + d) % N]; G4 offsets (k1_0 + d) * N + (c + d) % N.
+    int offd[DD], offg[DD];
 #pragma unroll
     for (int d = 0; d < DD; ++d) {
-        const int k1 = k1_0 + d;
-        rowok[d] = k1 < n;
-        colg[d] = wrap(c + d, n);
-        offd[d] = (rowok[d] ? k1 : 0) * n + colg[d];
+        const int k1 = wrap(k1_0 + d, n), k2 = wrap(c + d, n);
+        offd[d] = k1 * ld + k2;
+        offg[d] = k1 * n + k2;
     }
-    // Shifted operand offsets: stg[(q0 - k1_0 + m) % N][(q0 - c + m) % N],
-    // m = p - d in [-(DD-1), PP-1]  (q0, k1_0, c all in [0, N)).
+    // Shifted elements stg[(q0 - k1_0 + m) % N][(q0 - c + m) % N], m = p - d in [-(DD-1), PP-1].
     int offs[NS];
     {
         const int rb = wrap((int)(q0 - k1_0), n);
@@ -76,40 +101,42 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
 #pragma unroll
         for (int j = 0; j < NS; ++j) {
             const int m = j - (DD - 1);
-            offs[j] = wrap(rb + m, n) * n + wrap(cb + m, n);
+            offs[j] = wrap(rb + m, n) * ld + wrap(cb + m, n);
         }
     }
-
-    // Load the accumulator block.
-    Cx<R> acc[PP][DD];
-    bool ok[PP][DD];
-    Cx<R>* gp[PP][DD];
+    uint32_t okmask = 0;  // bit p*DD + d: entry belongs to the slice
 #pragma unroll
-    for (int p = 0; p < PP; ++p) {
-        const bool pok = (q0 + p) < P.hi;
-        const int64_t plane = (q0 + p - P.lo) * (int64_t)n;
+    for (int p = 0; p < PP; ++p)
+#pragma unroll
+        for (int d = 0; d < DD; ++d)
+            if (col_ok && (q0 + p) < P.hi && (k1_0 + d) < n) okmask |= 1u << (p * DD + d);
+
+    const int64_t nn = (int64_t)n * n;
+    Cx<R>* gb = P.g4 + (q0 - P.lo) * nn;
+    Cx<R> acc[PP][DD];
+#pragma unroll
+    for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int d = 0; d < DD; ++d) {
-            ok[p][d] = pok && rowok[d] && col_ok;
-            gp[p][d] = P.g4 + (plane + (rowok[d] ? k1_0 + d : 0)) * n + colg[d];
-            if (ok[p][d]) {
-                acc[p][d] = ld_g4(gp[p][d]);
+            if (okmask & (1u << (p * DD + d))) {
+                acc[p][d] = ld_g4(gb + p * nn + offg[d]);
             } else {
                 acc[p][d].re = R(0);
                 acc[p][d].im = R(0);
             }
         }
-    }
 
 #pragma unroll 1
     for (int w = 0; w < P.nbatch; ++w) {
-        const Stg<R>* s = P.stg[w];
+        const Cx<R>* su = P.stg[w];
+        const Cx<R>* sd = su + plane_s;
         Stg<R> dv[DD];
         Stg<R> sv[NS];
+        // all loads of the walker are issued before any math (memory-level parallelism)
 #pragma unroll
-        for (int d = 0; d < DD; ++d) dv[d] = ld_stg(s + offd[d]);
+        for (int d = 0; d < DD; ++d) dv[d] = ld_stg_v(su + offd[d], sd + offd[d]);
 #pragma unroll
-        for (int j = 0; j < NS; ++j) sv[j] = ld_stg(s + offs[j]);
+        for (int j = 0; j < NS; ++j) sv[j] = ld_stg_v(su + offs[j], sd + offs[j]);
 #pragma unroll
         for (int p = 0; p < PP; ++p) {
 #pragma unroll
@@ -129,27 +156,322 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
     for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int d = 0; d < DD; ++d)
-            if (ok[p][d]) st_g4(gp[p][d], acc[p][d]);
+            if (okmask & (1u << (p * DD + d))) st_g4(gb + p * nn + offg[d], acc[p][d]);
 }
 
-template <typename R, int PP, int DD, int WARPS>
-static g4_status launch_acc(const AccParams<R>& prm, cudaStream_t st) {
+template <typename R, int PP, int DD, int WARPS, int MINB>
+static g4_status launch_v1(const AccParams<R>& prm, cudaStream_t st) {
     const int n = prm.n;
-    const int64_t planes = prm.hi - prm.lo;
-    const int diag_blocks = (n + DD - 1) / DD;
-    dim3 grid((unsigned)((planes + PP - 1) / PP), (unsigned)((n + 31) / 32),
-              (unsigned)((diag_blocks + WARPS - 1) / WARPS));
+    const int64_t chunks = (prm.hi - prm.lo + PP - 1) / PP;
+    dim3 grid((unsigned)((chunks + WARPS - 1) / WARPS), (unsigned)((n + 31) / 32),
+              (unsigned)((n + DD - 1) / DD));
     if (grid.y > 65535u || grid.z > 65535u)
         return fail(G4_ERR_CONTRACT, "accumulate: N too large for the launch grid");
-    dim3 block(32, WARPS);
-    k_accumulate<R, PP, DD, WARPS><<<grid, block, 0, st>>>(prm);
+    k_accumulate<R, PP, DD, WARPS, MINB><<<grid, dim3(32, WARPS), 0, st>>>(prm);
     return check_cuda(cudaGetLastError(), "k_accumulate launch");
 }
 
+// ---------------------------------------------------------------------------
+// v2 -- TMA tensor boxes into a shared-memory ring (complex128).
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+// 3-D tensor box -> shared memory, completion counted on an mbarrier.
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ Stg<double> lds_stg(const Cx<double>* u, const Cx<double>* d) {
+    Stg<double> v;
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.ur), "=d"(v.ui) : "r"(smem_u32(u)));
+    asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.dr), "=d"(v.di) : "r"(smem_u32(d)));
+    return v;
+}
+
+constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel params)
+constexpr int V2_PP = 4, V2_DD = 4, V2_CW = 4, V2_NST = 4;
+constexpr int V2_DIRLEN = 32 + V2_DD - 1;                 // 35 direct columns
+constexpr int V2_NSH = V2_PP * V2_CW + V2_DD - 1;         // 19 shifted row segments
+constexpr int V2_DIR_ELEMS = V2_DD * V2_DIRLEN;           // per spin
+constexpr int V2_SH_ELEMS = V2_NSH * 32;                  // per spin
+constexpr uint32_t V2_DIR_BYTES = 2 * V2_DIR_ELEMS * 16;  // both spins, complex128
+constexpr uint32_t V2_SH_BYTES = 2 * V2_SH_ELEMS * 16;
+constexpr uint32_t V2_DIR_OFF = 0;
+constexpr uint32_t V2_SH_OFF = (V2_DIR_BYTES + 127) / 128 * 128;
+constexpr uint32_t V2_STAGE_BYTES = (V2_SH_OFF + V2_SH_BYTES + 127) / 128 * 128;
+constexpr size_t V2_SMEM = (size_t)V2_NST * V2_STAGE_BYTES + 2 * V2_NST * sizeof(uint64_t);
+static_assert(V2_NSH <= G4_HALO_ROWS && V2_NSH + 31 < G4_HALO_COLS, "halo too small for the v2 band");
+
+struct alignas(64) TmaParams {
+    CUtensorMap dmap[TMA_MAXW];  // direct tiles: plain 3-D map of the staged payload
+    CUtensorMap smap[TMA_MAXW];  // shifted bands: sheared 3-D map (row stride LD+1)
+    Cx<double>* g4;
+    int64_t lo, hi;
+    int32_t n;
+    int32_t nbatch;
+};
+
+__global__ void __launch_bounds__(32 * (V2_CW + 1), 2)
+k_accumulate_tma(const __grid_constant__ TmaParams P) {
+    constexpr int PP = V2_PP, DD = V2_DD;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)V2_NST * V2_STAGE_BYTES);
+    uint64_t* empty = full + V2_NST;
+
+    const int n = P.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t q0 = P.lo + (int64_t)blockIdx.x * (PP * V2_CW);
+    const int j0 = blockIdx.y * 32;
+    const int k1_0 = blockIdx.z * DD;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < V2_NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], V2_CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    if (warp == V2_CW) {
+        // ------------- producer: one lane issues two tensor boxes per walker -------------
+        if (lane == 0) {
+            // band origin: row R0 = (q0 - k1_0 - (DD-1)) mod N, column C0 = (q0 - j0 - 31 - (DD-1)) mod N;
+            // sheared coordinates (c1, c2) = (C0 - R0 + N, R0) (see make_maps).
+            const int R0 = wrap((int)(q0 - k1_0) - (DD - 1), n);
+            const int C0 = wrap((int)(q0 - j0) - 31 - (DD - 1), n);
+            for (int w = 0; w < P.nbatch; ++w) {
+                const int s = w % V2_NST;
+                if (w >= V2_NST) mbar_wait(&empty[s], ((w / V2_NST) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], V2_DIR_BYTES + V2_SH_BYTES);
+                unsigned char* st = smem_raw + (size_t)s * V2_STAGE_BYTES;
+                tma_load_3d(st + V2_DIR_OFF, &P.dmap[w], 2 * j0, k1_0, 0, &full[s]);
+                tma_load_3d(st + V2_SH_OFF, &P.smap[w], 2 * (C0 - R0 + n), R0, 0, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ------------- consumers: warp w owns planes q0 + 4w .. q0 + 4w + 3 -------------
+    const int c = j0 + lane;
+    const bool col_ok = c < n;
+    const int64_t nn = (int64_t)n * n;
+    const int64_t qw = q0 + PP * warp;
+    Cx<double>* gb = P.g4 + (qw - P.lo) * nn;
+    int offg[DD];
+#pragma unroll
+    for (int d = 0; d < DD; ++d) offg[d] = wrap(k1_0 + d, n) * n + wrap(c + d, n);
+    uint32_t okmask = 0;
+#pragma unroll
+    for (int p = 0; p < PP; ++p)
+#pragma unroll
+        for (int d = 0; d < DD; ++d)
+            if (col_ok && (qw + p) < P.hi && (k1_0 + d) < n) okmask |= 1u << (p * DD + d);
+    Cx<double> acc[PP][DD];
+#pragma unroll
+    for (int p = 0; p < PP; ++p)
+#pragma unroll
+        for (int d = 0; d < DD; ++d) {
+            if (okmask & (1u << (p * DD + d))) {
+                acc[p][d] = ld_g4(gb + p * nn + offg[d]);
+            } else {
+                acc[p][d].re = 0.0;
+                acc[p][d].im = 0.0;
+            }
+        }
+
+    // shared-memory element offsets (complex units) inside a stage
+    const int dir_o = lane;                           // + d * (DIRLEN + 1)
+    const int sh_o = (PP * warp) * 32 + (31 - lane);  // + j * 32
+#pragma unroll 1
+    for (int w = 0; w < P.nbatch; ++w) {
+        const int s = w % V2_NST;
+        mbar_wait(&full[s], (w / V2_NST) & 1);
+        const Cx<double>* dir_u =
+            reinterpret_cast<const Cx<double>*>(smem_raw + (size_t)s * V2_STAGE_BYTES + V2_DIR_OFF);
+        const Cx<double>* dir_d = dir_u + V2_DIR_ELEMS;
+        const Cx<double>* sh_u =
+            reinterpret_cast<const Cx<double>*>(smem_raw + (size_t)s * V2_STAGE_BYTES + V2_SH_OFF);
+        const Cx<double>* sh_d = sh_u + V2_SH_ELEMS;
+        Stg<double> dv[DD];
+        Stg<double> sv[PP + DD - 1];
+#pragma unroll
+        for (int d = 0; d < DD; ++d) {
+            const int o = dir_o + d * (V2_DIRLEN + 1);
+            dv[d] = lds_stg(dir_u + o, dir_d + o);
+        }
+#pragma unroll
+        for (int j = 0; j < PP + DD - 1; ++j) sv[j] = lds_stg(sh_u + sh_o + j * 32, sh_d + sh_o + j * 32);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+#pragma unroll
+        for (int p = 0; p < PP; ++p) {
+#pragma unroll
+            for (int d = 0; d < DD; ++d) {
+                const Stg<double>& S = sv[p - d + DD - 1];
+                const Stg<double>& D = dv[d];
+                double p1r, p1i, p2r, p2i;
+                cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);  // u * down[k2][k1]
+                cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);  // d * up[k2][k1]
+                acc[p][d].re = add_rn(acc[p][d].re, add_rn(p1r, p2r));
+                acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
+            }
+        }
+    }
+
+#pragma unroll
+    for (int p = 0; p < PP; ++p)
+#pragma unroll
+        for (int d = 0; d < DD; ++d)
+            if (okmask & (1u << (p * DD + d))) st_g4(gb + p * nn + offg[d], acc[p][d]);
+}
+
+// Host: tensor maps of one staged complex128 payload, cached by (pointer, n).
+using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                     const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                     const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                     CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+struct MapPair {
+    CUtensorMap dmap, smap;
+};
+
+static g4_status make_maps(const void* stg, int n, MapPair* out) {
+    static PFN_encodeTiled encode = nullptr;
+    if (!encode) {
+        cudaDriverEntryPointQueryResult q{};
+        void* fn = nullptr;
+        cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
+            return fail(G4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        encode = reinterpret_cast<PFN_encodeTiled>(fn);
+    }
+    const cuuint64_t ld = (cuuint64_t)staged_ld(n), rows = (cuuint64_t)staged_rows(n);
+    const cuuint64_t plane_b = (cuuint64_t)staged_plane(n) * 16;
+    const cuuint32_t estr[3] = {1, 1, 1};
+    // Rows are addressed as flat runs of doubles (re, im interleaved) so every box
+    // row is one contiguous 512-560 B transfer.
+    // direct: dims (doubles along a row, row, spin)
+    {
+        const cuuint64_t dims[3] = {2 * ld, rows, 2};
+        const cuuint64_t strides[2] = {ld * 16, plane_b};
+        const cuuint32_t box[3] = {2 * (cuuint32_t)V2_DIRLEN, (cuuint32_t)V2_DD, 2};
+        CUresult r = encode(&out->dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(stg), dims,
+                            strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled (direct) failed: %d", (int)r);
+            return G4_ERR_CUDA;
+        }
+    }
+    // sheared: element (x, c2) -> base - N*16 + x*8 + c2*(LD+1)*16, i.e. with
+    // x = 2*c1 + (0|1): stg[c2][c1 - N + c2] (row c2, column c1 - N + c2).
+    {
+        const cuuint64_t dims[3] = {2 * (2 * (cuuint64_t)n + ld), rows, 2};
+        const cuuint64_t strides[2] = {(ld + 1) * 16, plane_b};
+        const cuuint32_t box[3] = {64, (cuuint32_t)V2_NSH, 2};
+        void* base = static_cast<char*>(const_cast<void*>(stg)) - (size_t)n * 16;
+        CUresult r = encode(&out->smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) {
+            set_error("cuTensorMapEncodeTiled (sheared) failed: %d", (int)r);
+            return G4_ERR_CUDA;
+        }
+    }
+    return G4_OK;
+}
+
+static g4_status get_maps(const void* stg, int n, MapPair* out) {
+    static std::mutex mu;
+    static std::unordered_map<uint64_t, MapPair> cache;
+    const uint64_t key = reinterpret_cast<uint64_t>(stg) ^ ((uint64_t)n << 48);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return G4_OK;
+    }
+    G4_TRY(make_maps(stg, n, out));
+    if (cache.size() > 4096) cache.clear();
+    cache.emplace(key, *out);
+    return G4_OK;
+}
+
+static g4_status launch_v2(const AccParams<double>& prm, cudaStream_t st) {
+    static bool attr_set = false;
+    if (!attr_set) {
+        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)V2_SMEM));
+        attr_set = true;
+    }
+    const int n = prm.n;
+    for (int b0 = 0; b0 < prm.nbatch; b0 += TMA_MAXW) {
+        TmaParams tp;
+        std::memset(&tp, 0, sizeof(tp));
+        tp.g4 = prm.g4;
+        tp.lo = prm.lo;
+        tp.hi = prm.hi;
+        tp.n = n;
+        tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
+        for (int i = 0; i < tp.nbatch; ++i) {
+            MapPair mp;
+            G4_TRY(get_maps(prm.stg[b0 + i], n, &mp));
+            tp.dmap[i] = mp.dmap;
+            tp.smap[i] = mp.smap;
+        }
+        const int64_t planes = prm.hi - prm.lo;
+        dim3 grid((unsigned)((planes + V2_PP * V2_CW - 1) / (V2_PP * V2_CW)), (unsigned)((n + 31) / 32),
+                  (unsigned)((n + V2_DD - 1) / V2_DD));
+        if (grid.y > 65535u || grid.z > 65535u)
+            return fail(G4_ERR_CONTRACT, "accumulate: N too large for the launch grid");
+        k_accumulate_tma<<<grid, 32 * (V2_CW + 1), V2_SMEM, st>>>(tp);
+        G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
+    }
+    return G4_OK;
+}
+
+// ---------------------------------------------------------------------------
 template <typename R>
-static g4_status accumulate_t(void* g4p, int64_t lo, int64_t hi, int32_t n,
-                              const void* const* staged, int32_t nbatch, cudaStream_t st) {
-    const uintptr_t stg_align = sizeof(Stg<R>);
+static g4_status dispatch(const AccParams<R>& prm, cudaStream_t st) {
+    const int64_t planes = prm.hi - prm.lo;
+    const int variant = kernel_variant();
+    if constexpr (sizeof(R) == 8) {
+        if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2(prm, st);
+        if (variant == 2 && prm.n >= 64) return launch_v2(prm, st);
+    }
+    if (planes <= 4) return launch_v1<R, 4, 4, 1, 12>(prm, st);
+    if (planes <= 8) return launch_v1<R, 4, 4, 2, 6>(prm, st);
+    return launch_v1<R, 4, 4, 4, 3>(prm, st);
+}
+
+template <typename R>
+static g4_status accumulate_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                              int32_t nbatch, cudaStream_t st) {
     if (!aligned(g4p, sizeof(Cx<R>)))
         return fail(G4_ERR_CONTRACT, "accumulate: g4 slice pointer is not entry-aligned");
     for (int32_t b0 = 0; b0 < nbatch; b0 += G4_MAX_BATCH) {
@@ -162,11 +484,10 @@ static g4_status accumulate_t(void* g4p, int64_t lo, int64_t hi, int32_t n,
         for (int i = 0; i < prm.nbatch; ++i) {
             const void* sp = staged[b0 + i];
             if (!sp) return fail(G4_ERR_CONTRACT, "accumulate: null staged payload");
-            if (!aligned(sp, stg_align))
-                return fail(G4_ERR_CONTRACT, "accumulate: staged payload is not 32B/16B aligned");
-            prm.stg[i] = static_cast<const Stg<R>*>(sp);
+            if (!aligned(sp, 16)) return fail(G4_ERR_CONTRACT, "accumulate: staged payload is not 16-B aligned");
+            prm.stg[i] = static_cast<const Cx<R>*>(sp);
         }
-        G4_TRY((launch_acc<R, 4, 4, 4>(prm, st)));
+        G4_TRY(dispatch(prm, st));
     }
     return G4_OK;
 }
@@ -175,9 +496,8 @@ static g4_status accumulate_t(void* g4p, int64_t lo, int64_t hi, int32_t n,
 
 extern "C" {
 
-g4_status g4_accumulate_staged(void* g4p, int64_t lo, int64_t hi, int32_t n,
-                               const void* const* staged, int32_t nbatch, int32_t dtype,
-                               int32_t channel, void* stream) {
+g4_status g4_accumulate_staged(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                               int32_t nbatch, int32_t dtype, int32_t channel, void* stream) {
     using namespace g4;
     if (n < 1) return fail(G4_ERR_CONTRACT, "index space size must be >= 1");
     if (!(0 <= lo && lo < hi && hi <= n)) {
@@ -195,6 +515,13 @@ g4_status g4_accumulate_staged(void* g4p, int64_t lo, int64_t hi, int32_t n,
     return fail(G4_ERR_CONTRACT, "unknown dtype");
 }
 
+g4_status g4_set_kernel_variant(int32_t variant) {
+    if (variant < 0 || variant > 2)
+        return g4::fail(G4_ERR_CONTRACT, "kernel variant must be 0 (auto), 1 (v1) or 2 (v2)");
+    g4::g_variant = variant;
+    return G4_OK;
+}
+
 int64_t g4_accumulate_workspace_bytes(int32_t n, int32_t nbatch, int32_t dtype) {
     const int64_t pb = g4_payload_bytes(n, dtype);
     if (pb < 0 || nbatch < 0) return -1;
@@ -209,8 +536,7 @@ g4_status g4_accumulate(void* g4p, int64_t lo, int64_t hi, int32_t n, const void
     if (nbatch == 0) return g4_accumulate_staged(g4p, lo, hi, n, nullptr, 0, dtype, channel, stream);
     const int64_t need = g4_accumulate_workspace_bytes(n, nbatch, dtype);
     if (need < 0) return fail(G4_ERR_CONTRACT, "accumulate: bad n/dtype");
-    if (!workspace || workspace_bytes < need)
-        return fail(G4_ERR_CONTRACT, "accumulate: workspace too small");
+    if (!workspace || workspace_bytes < need) return fail(G4_ERR_CONTRACT, "accumulate: workspace too small");
     const int64_t pb = g4_payload_bytes(n, dtype);
     void* stg[G4_MAX_BATCH];
     for (int32_t b0 = 0; b0 < nbatch; b0 += G4_MAX_BATCH) {

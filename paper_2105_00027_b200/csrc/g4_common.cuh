@@ -9,6 +9,8 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+#include "../../include/g4ring.h"
+
 namespace g4 {
 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
@@ -25,31 +27,58 @@ __device__ __forceinline__ void cmul(R xr, R xi, R yr, R yi, R& zr, R& zi) {
     zi = fma_rn(xr, yi, mul_rn(xi, yr));
 }
 
-// One staged walker element: (u, d) = (up^T, down^T) at one (row, col).
-// Staged layout of one walker: stg[r * N + c] = { up[c][r], down[c][r] }, so the
-// accumulate kernel reads both spins of both operands row-contiguously.
-template <typename R>
-struct alignas(4 * sizeof(R)) Stg {
-    R ur, ui, dr, di;
-};
-
 // One G4 entry (complex).
 template <typename R>
 struct alignas(2 * sizeof(R)) Cx {
     R re, im;
 };
 
-// 256-bit (c128) / 128-bit (c64) read-only loads of a staged element.
-__device__ __forceinline__ Stg<double> ld_stg(const Stg<double>* p) {
+// Staged layout of one walker payload in memory (include/g4ring.h): spin-planar
+// transposes with a cyclic halo,
+//   stg[s][r][c] = M_s[c mod N][r mod N],  s = 0 (up), 1 (down),
+//   r < ROWS = N + G4_HALO_ROWS,  c < LD = N + G4_HALO_COLS,
+// so every operand row of the update is contiguous, every 16-B (c128) half is
+// a contiguous stream in global and shared memory, and any window of up to
+// HALO rows / cols starting inside the core never wraps (TMA boxes).
+__host__ __device__ __forceinline__ int staged_ld(int n) { return n + G4_HALO_COLS; }
+__host__ __device__ __forceinline__ int staged_rows(int n) { return n + G4_HALO_ROWS; }
+__host__ __device__ __forceinline__ int64_t staged_plane(int n) {
+    return (int64_t)staged_rows(n) * staged_ld(n);
+}
+
+// One staged walker element in registers: (u, d) = (up^T, down^T) at one (row, col).
+template <typename R>
+struct Stg {
+    R ur, ui, dr, di;
+};
+
+
+// Read-only loads of a staged element: u from the up^T plane, d from the down^T plane.
+__device__ __forceinline__ Stg<double> ld_stg(const Cx<double>* u, const Cx<double>* d) {
     Stg<double> v;
-    asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
-                 : "=d"(v.ur), "=d"(v.ui), "=d"(v.dr), "=d"(v.di) : "l"(p));
+    asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.ur), "=d"(v.ui) : "l"(u));
+    asm("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.dr), "=d"(v.di) : "l"(d));
     return v;
 }
-__device__ __forceinline__ Stg<float> ld_stg(const Stg<float>* p) {
+__device__ __forceinline__ Stg<float> ld_stg(const Cx<float>* u, const Cx<float>* d) {
     Stg<float> v;
-    asm volatile("ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%4];"
-                 : "=f"(v.ur), "=f"(v.ui), "=f"(v.dr), "=f"(v.di) : "l"(p));
+    asm("ld.global.nc.v2.f32 {%0,%1}, [%2];" : "=f"(v.ur), "=f"(v.ui) : "l"(u));
+    asm("ld.global.nc.v2.f32 {%0,%1}, [%2];" : "=f"(v.dr), "=f"(v.di) : "l"(d));
+    return v;
+}
+
+// Same, as volatile asm: the walker's loads keep their program order ahead of
+// the math that consumes them, so all of them are in flight at once.
+__device__ __forceinline__ Stg<double> ld_stg_v(const Cx<double>* u, const Cx<double>* d) {
+    Stg<double> v;
+    asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.ur), "=d"(v.ui) : "l"(u));
+    asm volatile("ld.global.nc.v2.f64 {%0,%1}, [%2];" : "=d"(v.dr), "=d"(v.di) : "l"(d));
+    return v;
+}
+__device__ __forceinline__ Stg<float> ld_stg_v(const Cx<float>* u, const Cx<float>* d) {
+    Stg<float> v;
+    asm volatile("ld.global.nc.v2.f32 {%0,%1}, [%2];" : "=f"(v.ur), "=f"(v.ui) : "l"(u));
+    asm volatile("ld.global.nc.v2.f32 {%0,%1}, [%2];" : "=f"(v.dr), "=f"(v.di) : "l"(d));
     return v;
 }
 

@@ -10,50 +10,54 @@ namespace g4 {
 constexpr int MAXB = G4_MAX_BATCH;
 
 // ---------------------------------------------------------------------------
-// K2: staged[r][c] = { up[c][r], down[c][r] }  -- a 32x32-tile transpose of both
-// spins through shared memory; coalesced reads of up/down rows, coalesced
-// 256-bit (c128) writes of staged rows.  blockIdx.z = walker.
+// K2: staged[0][r][c] = up[c][r], staged[1][r][c] = down[c][r] -- a 32x32-tile
+// transpose of both spins through shared memory; coalesced reads of up/down
+// rows, coalesced writes of staged rows.  blockIdx.z = walker.
 template <typename Rin, typename Rout>
 struct PrepParams {
     const Cx<Rin>* up[MAXB];
     const Cx<Rin>* down[MAXB];
-    Stg<Rout>* stg[MAXB];
+    Cx<Rout>* stg[MAXB];  // spin-planar staged output (2 x N x N)
     int32_t n;
 };
 
 template <typename Rin, typename Rout>
 __global__ void __launch_bounds__(256) k_prepare(const __grid_constant__ PrepParams<Rin, Rout> P) {
+    // staged tile rows r0.. / cols c0.. of the padded layout; sources are the
+    // reference rows (c0 + i) mod N, columns (r0 + j) mod N.
     __shared__ Cx<Rin> su[32][33];
     __shared__ Cx<Rin> sd[32][33];
     const int n = P.n;
+    const int ld = staged_ld(n), rows = staged_rows(n);
     const int w = blockIdx.z;
     const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     const Cx<Rin>* up = P.up[w];
     const Cx<Rin>* dn = P.down[w];
-    // read rows c0.. of up/down (columns r0..), i.e. up[c][r]
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int c = c0 + threadIdx.y + 8 * i, r = r0 + threadIdx.x;
-        if (c < n && r < n) {
-            const int64_t o = (int64_t)c * n + r;
+        if (c < ld && r < rows) {
+            const int64_t o = (int64_t)(c % n) * n + (r % n);
             su[threadIdx.y + 8 * i][threadIdx.x] = up[o];
             sd[threadIdx.y + 8 * i][threadIdx.x] = dn[o];
         }
     }
     __syncthreads();
-    Stg<Rout>* out = P.stg[w];
+    Cx<Rout>* out_u = P.stg[w];
+    Cx<Rout>* out_d = out_u + staged_plane(n);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
         const int r = r0 + threadIdx.y + 8 * i, c = c0 + threadIdx.x;
-        if (c < n && r < n) {
+        if (c < ld && r < rows) {
             const Cx<Rin> u = su[threadIdx.x][threadIdx.y + 8 * i];
             const Cx<Rin> d = sd[threadIdx.x][threadIdx.y + 8 * i];
-            Stg<Rout> v;
-            v.ur = (Rout)u.re;
-            v.ui = (Rout)u.im;
-            v.dr = (Rout)d.re;
-            v.di = (Rout)d.im;
-            out[(int64_t)r * n + c] = v;
+            Cx<Rout> vu, vd;
+            vu.re = (Rout)u.re;
+            vu.im = (Rout)u.im;
+            vd.re = (Rout)d.re;
+            vd.im = (Rout)d.im;
+            out_u[(int64_t)r * ld + c] = vu;
+            out_d[(int64_t)r * ld + c] = vd;
         }
     }
 }
@@ -67,17 +71,17 @@ static g4_status prepare_t(void* const* staged, const void* const* up, const voi
         for (int i = 0; i < nb; ++i) {
             if (!staged[b0 + i] || !up[b0 + i] || !down[b0 + i])
                 return fail(G4_ERR_CONTRACT, "prepare_g: null pointer");
-            if (!aligned(staged[b0 + i], sizeof(Stg<Rout>)) || !aligned(up[b0 + i], sizeof(Cx<Rin>)) ||
+            if (!aligned(staged[b0 + i], sizeof(Cx<Rout>)) || !aligned(up[b0 + i], sizeof(Cx<Rin>)) ||
                 !aligned(down[b0 + i], sizeof(Cx<Rin>)))
                 return fail(G4_ERR_CONTRACT, "prepare_g: misaligned payload pointer");
             prm.up[i] = static_cast<const Cx<Rin>*>(up[b0 + i]);
             prm.down[i] = static_cast<const Cx<Rin>*>(down[b0 + i]);
-            prm.stg[i] = static_cast<Stg<Rout>*>(staged[b0 + i]);
+            prm.stg[i] = static_cast<Cx<Rout>*>(staged[b0 + i]);
         }
         prm.n = n;
-        const unsigned t = (unsigned)((n + 31) / 32);
-        if (t > 65535u) return fail(G4_ERR_CONTRACT, "prepare_g: N too large");
-        k_prepare<Rin, Rout><<<dim3(t, t, nb), dim3(32, 8), 0, st>>>(prm);
+        const unsigned tr = (unsigned)((staged_rows(n) + 31) / 32), tc = (unsigned)((staged_ld(n) + 31) / 32);
+        if (tr > 65535u || tc > 65535u) return fail(G4_ERR_CONTRACT, "prepare_g: N too large");
+        k_prepare<Rin, Rout><<<dim3(tr, tc, nb), dim3(32, 8), 0, st>>>(prm);
         G4_CUDA(cudaGetLastError());
     }
     return G4_OK;
@@ -91,7 +95,7 @@ static g4_status prepare_t(void* const* staged, const void* const* up, const voi
 //   integer: value = (floor(5 u1) - 2, floor(5 u2) - 2)                  (tensor.py:204-209)
 template <typename R>
 struct GenParams {
-    Stg<R>* stg[MAXB];
+    Cx<R>* stg[MAXB];
     Cx<R>* up[MAXB];
     Cx<R>* down[MAXB];
     uint64_t key_up[MAXB];
@@ -118,24 +122,27 @@ __device__ __forceinline__ void gen_entry(uint64_t key, uint64_t idx, int mode, 
     }
 }
 
-// Staged output: thread (r, c) with c fastest -> stg[r][c] = {up[c][r], down[c][r]};
-// entry index of up[c][r] is c*N + r.
+// Staged output: thread (r, c) of the padded layout, c fastest ->
+// stg[0][r][c] = up[c mod N][r mod N], stg[1][r][c] = down[c mod N][r mod N]
+// (entry index of up[c'][r'] is c'*N + r'; halo entries are regenerated).
 template <typename R>
 __global__ void __launch_bounds__(256) k_generate_staged(const __grid_constant__ GenParams<R> P) {
     const int n = P.n, w = blockIdx.z;
+    const int ld = staged_ld(n), rows = staged_rows(n);
     const int c = blockIdx.x * 32 + threadIdx.x;
     const int r = blockIdx.y * 8 + threadIdx.y;
-    if (c >= n || r >= n) return;
-    const uint64_t idx = (uint64_t)c * n + r;
+    if (c >= ld || r >= rows) return;
+    const uint64_t idx = (uint64_t)(c % n) * n + (r % n);
     double ur, ui, dr, di;
     gen_entry(P.key_up[w], idx, P.mode, ur, ui);
     gen_entry(P.key_down[w], idx, P.mode, dr, di);
-    Stg<R> v;
-    v.ur = (R)ur;
-    v.ui = (R)ui;
-    v.dr = (R)dr;
-    v.di = (R)di;
-    P.stg[w][(int64_t)r * n + c] = v;
+    Cx<R> vu, vd;
+    vu.re = (R)ur;
+    vu.im = (R)ui;
+    vd.re = (R)dr;
+    vd.im = (R)di;
+    P.stg[w][(int64_t)r * ld + c] = vu;
+    P.stg[w][staged_plane(n) + (int64_t)r * ld + c] = vd;
 }
 
 // Reference-layout output: thread per row-major entry idx.
@@ -181,10 +188,10 @@ static g4_status generate_t(void* const* staged, void* const* up, void* const* d
             const int j = b0 + i;
             prm.key_up[i] = stream_key(seed, wr[j], lane[j], meas[j], 0);
             prm.key_down[i] = stream_key(seed, wr[j], lane[j], meas[j], 1);
-            prm.stg[i] = staged ? static_cast<Stg<R>*>(staged[j]) : nullptr;
+            prm.stg[i] = staged ? static_cast<Cx<R>*>(staged[j]) : nullptr;
             prm.up[i] = up ? static_cast<Cx<R>*>(up[j]) : nullptr;
             prm.down[i] = down ? static_cast<Cx<R>*>(down[j]) : nullptr;
-            if (prm.stg[i] && !aligned(prm.stg[i], sizeof(Stg<R>)))
+            if (prm.stg[i] && !aligned(prm.stg[i], sizeof(Cx<R>)))
                 return fail(G4_ERR_CONTRACT, "generate: misaligned staged pointer");
             any_stg |= prm.stg[i] != nullptr;
             any_ref |= (prm.up[i] != nullptr) || (prm.down[i] != nullptr);
@@ -192,7 +199,7 @@ static g4_status generate_t(void* const* staged, void* const* up, void* const* d
         if (any_stg) {
             for (int i = 0; i < nb; ++i)
                 if (!prm.stg[i]) return fail(G4_ERR_CONTRACT, "generate: staged list has a null entry");
-            dim3 grid((unsigned)((n + 31) / 32), (unsigned)((n + 7) / 8), nb);
+            dim3 grid((unsigned)((staged_ld(n) + 31) / 32), (unsigned)((staged_rows(n) + 7) / 8), nb);
             if (grid.y > 65535u) return fail(G4_ERR_CONTRACT, "generate: N too large");
             k_generate_staged<R><<<grid, dim3(32, 8), 0, st>>>(prm);
             G4_CUDA(cudaGetLastError());

@@ -23,9 +23,10 @@ oracle_accumulate      oracle_accumulate         (276-283)   K3 + K1 in canonica
 Differences, all deliberate:
 * ``GtSlice.data`` is a CUDA ``torch.Tensor`` (complex128, or complex64) with the
   reference's exact layout ``data[k3 - lo, k1, k2]``.
-* ``GSigma`` stores one device tensor ``staged`` of shape (N, N, 2):
-  ``staged[r, c] = (up[c, r], down[c, r])`` -- the layout the update kernel reads
-  row-contiguously and the form that travels around the ring.  ``g.up`` and
+* ``GSigma`` stores one device tensor ``staged`` of shape (2, N + 32, N + 64):
+  spin-planar transposes with a cyclic halo, ``staged[s, r, c] = M_s[c % N, r % N]``
+  (``M_0 = up``, ``M_1 = down``) -- the layout the update kernel reads
+  row-contiguously (and with TMA boxes) and the form that travels around the ring.  ``g.up`` and
   ``g.down`` are (transposed, zero-copy) views with the reference's meaning.
 * There is no CPU path: host arrays passed in are copied to the device; a
   missing CUDA library raises ``LibraryUnavailable``.
@@ -45,6 +46,11 @@ ENTRY_BYTES = 16  # complex128 (tensor.py:23)
 VALUE_MODES = ("float", "integer")
 _MODE_CODE = {"float": _lib.G4_MODE_FLOAT, "integer": _lib.G4_MODE_INTEGER}
 _DTYPE_CODE = {torch.complex128: _lib.G4_C128, torch.complex64: _lib.G4_C64}
+
+
+def staged_shape(n: int) -> tuple[int, int, int]:
+    """Shape of one staged payload (include/g4ring.h): (2, N + HALO_ROWS, N + HALO_COLS)."""
+    return (2, n + _lib.G4_HALO_ROWS, n + _lib.G4_HALO_COLS)
 
 
 def _stream_ptr(device: torch.device) -> int:
@@ -124,13 +130,13 @@ class GSigma:
         n = space.size
         if staged is not None:
             _require_cuda(staged, "GSigma.staged")
-            if tuple(staged.shape) != (n, n, 2) or not staged.is_contiguous():
-                raise ContractViolation(f"staged payload must be contiguous ({n}, {n}, 2)")
+            if tuple(staged.shape) != staged_shape(n) or not staged.is_contiguous():
+                raise ContractViolation(f"staged payload must be contiguous {staged_shape(n)}")
             _dtype_code(staged.dtype)
             self.staged = staged
             return
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.staged = torch.empty((n, n, 2), dtype=dtype, device=dev)
+        self.staged = torch.empty(staged_shape(n), dtype=dtype, device=dev)
         if up is None and down is None:
             self.staged.zero_()
             return
@@ -139,11 +145,13 @@ class GSigma:
     # -- reference-meaning accessors (zero-copy views) --------------------------
     @property
     def up(self) -> torch.Tensor:
-        return self.staged[:, :, 0].transpose(0, 1)
+        n = self.space.size
+        return self.staged[0, :n, :n].transpose(0, 1)
 
     @property
     def down(self) -> torch.Tensor:
-        return self.staged[:, :, 1].transpose(0, 1)
+        n = self.space.size
+        return self.staged[1, :n, :n].transpose(0, 1)
 
     @property
     def dtype(self) -> torch.dtype:
@@ -151,7 +159,13 @@ class GSigma:
 
     @property
     def nbytes(self) -> int:
+        """Reference payload size (tensor.py:86-89): two N x N matrices."""
         return 2 * self.space.size ** 2 * self.staged.element_size()
+
+    @property
+    def device_nbytes(self) -> int:
+        """Bytes of the staged device payload (core + halo)."""
+        return self.staged.numel() * self.staged.element_size()
 
     def set(self, up, down) -> None:
         """Stage reference-layout matrices (numpy or torch, host or device) with K2."""

@@ -64,6 +64,18 @@ def test_random_shapes_bitwise_vs_oracle(oracle, cuda_dev, n, lo, hi, nb):
     assert np.array_equal(to_np(sl.data), ref)
 
 
+@pytest.mark.parametrize("variant", [0, 1, 2])
+@pytest.mark.parametrize("n,lo,hi,nb", [(64, 3, 64, 9), (100, 0, 17, 4), (257, 250, 257, 6),
+                                        (512, 500, 512, 5), (200, 0, 5, 3), (67, 60, 67, 2)])
+def test_both_kernel_variants_bitwise(oracle, cuda_dev, variant, n, lo, hi, nb):
+    lib = _lib.load()
+    _lib.check(lib.g4_set_kernel_variant(variant))
+    try:
+        test_random_shapes_bitwise_vs_oracle(oracle, cuda_dev, n, lo, hi, nb)
+    finally:
+        _lib.check(lib.g4_set_kernel_variant(0))
+
+
 def test_config1_device_generator(golden, cuda_dev):
     """BASELINE config 1: N=32, K3={0}, 16 walkers generated on the device."""
     c1 = golden("c1.npz")
@@ -107,7 +119,10 @@ def test_prepare_is_exact_transpose(cuda_dev):
         down = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
         g = payload(up, down, cuda_dev)
         st = to_np(g.staged)
-        assert np.array_equal(st[:, :, 0], up.T) and np.array_equal(st[:, :, 1], down.T)
+        assert st.shape == T.staged_shape(n)
+        assert np.array_equal(st[0, :n, :n], up.T) and np.array_equal(st[1, :n, :n], down.T)
+        rr, cc = np.meshgrid(np.arange(st.shape[1]) % n, np.arange(st.shape[2]) % n, indexing="ij")
+        assert np.array_equal(st[0], up.T[rr, cc]) and np.array_equal(st[1], down.T[rr, cc])  # halo
         assert np.array_equal(to_np(g.up.contiguous()), up)
 
 
@@ -228,7 +243,7 @@ def test_c128_payload_staged_as_c64(cuda_dev):
     up = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
     down = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
     g = payload(up, down, cuda_dev, dtype=torch.complex64)
-    assert np.array_equal(to_np(g.staged)[:, :, 0], up.T.astype(np.complex64))
+    assert np.array_equal(to_np(g.staged)[0, :n, :n], up.T.astype(np.complex64))
 
 
 def test_reduce_sum_canonical_order(cuda_dev):
