@@ -21,9 +21,9 @@
 //
 // v1 (k_accumulate): CTA = WARPS warps stacked along K3 (they share the direct
 //    elements and most shifted rows through L1); loads straight from global.
-// v2 (k_accumulate_tma, complex128, N >= 64): warp-specialised.  One producer
-//    lane streams, per walker, two TMA tensor boxes into a 4-stage shared-memory
-//    ring: the CTA's direct tile (4 rows x 35 cols x 2 spins) through a plain
+// v2 (k_accumulate_tma, complex128, N >= 64): one producer lane (lane 0 of
+//    warp 0, which is also a consumer) streams, per walker, two TMA tensor boxes
+//    into a 3-stage shared-memory ring (3 CTAs per SM): the CTA's direct tile (4 rows x 35 cols x 2 spins) through a plain
 //    tensor map, and its whole shifted band (19 diagonal row segments x 32
 //    cols x 2 spins) through a *sheared* tensor map (row stride LD+1 elements)
 //    that turns the diagonal band into a rectangular box.  The halo of the
@@ -213,7 +213,7 @@ __device__ __forceinline__ Stg<double> lds_stg(const Cx<double>* u, const Cx<dou
 }
 
 constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel params)
-constexpr int V2_PP = 4, V2_DD = 4, V2_CW = 4, V2_NST = 4;
+constexpr int V2_PP = 4, V2_DD = 4, V2_CW = 4, V2_NST = 3;
 constexpr int V2_DIRLEN = 32 + V2_DD - 1;                 // 35 direct columns
 constexpr int V2_NSH = V2_PP * V2_CW + V2_DD - 1;         // 19 shifted row segments
 constexpr int V2_DIR_ELEMS = V2_DD * V2_DIRLEN;           // per spin
@@ -235,7 +235,7 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
 };
 
-__global__ void __launch_bounds__(32 * (V2_CW + 1), 2)
+__global__ void __launch_bounds__(32 * V2_CW, 3)
 k_accumulate_tma(const __grid_constant__ TmaParams P) {
     constexpr int PP = V2_PP, DD = V2_DD;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -247,36 +247,30 @@ k_accumulate_tma(const __grid_constant__ TmaParams P) {
     const int64_t q0 = P.lo + (int64_t)blockIdx.x * (PP * V2_CW);
     const int j0 = blockIdx.y * 32;
     const int k1_0 = blockIdx.z * DD;
+    const bool producer = threadIdx.x == 0;
+    // band origin: row R0 = (q0 - k1_0 - (DD-1)) mod N, column C0 = (q0 - j0 - 31 - (DD-1)) mod N;
+    // sheared coordinates (c1, c2) = (C0 - R0 + N, R0) (see make_maps).
+    const int R0 = wrap((int)(q0 - k1_0) - (DD - 1), n);
+    const int C0 = wrap((int)(q0 - j0) - 31 - (DD - 1), n);
+    auto issue = [&](int w) {  // producer lane: both tensor boxes of walker w into stage w % NST
+        const int s = w % V2_NST;
+        mbar_arrive_expect_tx(&full[s], V2_DIR_BYTES + V2_SH_BYTES);
+        unsigned char* st = smem_raw + (size_t)s * V2_STAGE_BYTES;
+        tma_load_3d(st + V2_DIR_OFF, &P.dmap[w], 2 * j0, k1_0, 0, &full[s]);
+        tma_load_3d(st + V2_SH_OFF, &P.smap[w], 2 * (C0 - R0 + n), R0, 0, &full[s]);
+    };
 
-    if (threadIdx.x == 0) {
+    if (producer) {
         for (int s = 0; s < V2_NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], V2_CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int w = 0; w < V2_NST && w < P.nbatch; ++w) issue(w);
     }
     __syncthreads();
 
-    if (warp == V2_CW) {
-        // ------------- producer: one lane issues two tensor boxes per walker -------------
-        if (lane == 0) {
-            // band origin: row R0 = (q0 - k1_0 - (DD-1)) mod N, column C0 = (q0 - j0 - 31 - (DD-1)) mod N;
-            // sheared coordinates (c1, c2) = (C0 - R0 + N, R0) (see make_maps).
-            const int R0 = wrap((int)(q0 - k1_0) - (DD - 1), n);
-            const int C0 = wrap((int)(q0 - j0) - 31 - (DD - 1), n);
-            for (int w = 0; w < P.nbatch; ++w) {
-                const int s = w % V2_NST;
-                if (w >= V2_NST) mbar_wait(&empty[s], ((w / V2_NST) - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], V2_DIR_BYTES + V2_SH_BYTES);
-                unsigned char* st = smem_raw + (size_t)s * V2_STAGE_BYTES;
-                tma_load_3d(st + V2_DIR_OFF, &P.dmap[w], 2 * j0, k1_0, 0, &full[s]);
-                tma_load_3d(st + V2_SH_OFF, &P.smap[w], 2 * (C0 - R0 + n), R0, 0, &full[s]);
-            }
-        }
-        return;
-    }
-
-    // ------------- consumers: warp w owns planes q0 + 4w .. q0 + 4w + 3 -------------
+    // ------------- warp w owns planes q0 + 4w .. q0 + 4w + 3 -------------
     const int c = j0 + lane;
     const bool col_ok = c < n;
     const int64_t nn = (int64_t)n * n;
@@ -326,8 +320,13 @@ k_accumulate_tma(const __grid_constant__ TmaParams P) {
         }
 #pragma unroll
         for (int j = 0; j < PP + DD - 1; ++j) sv[j] = lds_stg(sh_u + sh_o + j * 32, sh_d + sh_o + j * 32);
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        // Producer duty (lane 0 of warp 0): refill the stage every warp released in
+        // the previous iteration with walker w - 1 + NST; its TMA overlaps this math.
+        if (producer && w >= 1 && w - 1 + V2_NST < P.nbatch) {
+            const int wp = w - 1;
+            mbar_wait(&empty[wp % V2_NST], (wp / V2_NST) & 1);
+            issue(wp + V2_NST);
+        }
 #pragma unroll
         for (int p = 0; p < PP; ++p) {
 #pragma unroll
@@ -341,6 +340,10 @@ k_accumulate_tma(const __grid_constant__ TmaParams P) {
                 acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
             }
         }
+        // Release the stage only once its values have been consumed by the math
+        // (an in-flight ld.shared must not race the TMA refill of the stage).
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
     }
 
 #pragma unroll
@@ -449,7 +452,7 @@ static g4_status launch_v2(const AccParams<double>& prm, cudaStream_t st) {
                   (unsigned)((n + V2_DD - 1) / V2_DD));
         if (grid.y > 65535u || grid.z > 65535u)
             return fail(G4_ERR_CONTRACT, "accumulate: N too large for the launch grid");
-        k_accumulate_tma<<<grid, 32 * (V2_CW + 1), V2_SMEM, st>>>(tp);
+        k_accumulate_tma<<<grid, 32 * V2_CW, V2_SMEM, st>>>(tp);
         G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
     }
     return G4_OK;
