@@ -133,9 +133,14 @@ g4_status g4_accumulate(void* g4, int64_t lo, int64_t hi, int32_t n, const void*
 
 #define G4_IPC_HANDLE_BYTES 64
 
-/* Export / import a device allocation between processes (cudaIpc*MemHandle). */
-g4_status g4_ipc_export(void* dev_ptr, void* handle_out /* G4_IPC_HANDLE_BYTES */);
-g4_status g4_ipc_import(const void* handle, void** dev_ptr_out);
+/* Export a device pointer to other processes: the CUDA IPC handle of the
+ * allocation containing it (G4_IPC_HANDLE_BYTES) and its byte offset inside
+ * that allocation (pointers from a caching allocator are sub-allocations). */
+g4_status g4_ipc_export(void* dev_ptr, void* handle_out, int64_t* offset_out);
+/* Map an exported pointer into this process (reference counted per allocation;
+ * works across GPUs over NVLink and between processes sharing one GPU). */
+g4_status g4_ipc_import(const void* handle, int64_t offset, void** dev_ptr_out);
+/* Release a pointer returned by g4_ipc_import. */
 g4_status g4_ipc_close(void* dev_ptr);
 
 /* Stream-ordered peer copy (copy engine over NVLink/NVSwitch, or local). */

@@ -41,8 +41,8 @@ SIGNATURES = {
     "g4_set_kernel_variant": (_i32, [_i32]),
     "g4_accumulate_workspace_bytes": (_i64, [_i32, _i32, _i32]),
     "g4_accumulate": (_i32, [_vp, _i64, _i64, _i32, _vpp, _vpp, _i32, _i32, _i32, _vp, _i64, _vp]),
-    "g4_ipc_export": (_i32, [_vp, _vp]),
-    "g4_ipc_import": (_i32, [_vp, _vpp]),
+    "g4_ipc_export": (_i32, [_vp, _vp, _i64p]),
+    "g4_ipc_import": (_i32, [_vp, _i64, _vpp]),
     "g4_ipc_close": (_i32, [_vp]),
     "g4_copy_async": (_i32, [_vp, _vp, _i64, _vp]),
     "g4_flag_write": (_i32, [_vp, _u64, _vp]),

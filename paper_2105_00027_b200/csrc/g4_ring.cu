@@ -8,6 +8,9 @@
 #include <algorithm>
 #include <chrono>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
 #include <thread>
 
 #include <cuda.h>
@@ -21,6 +24,7 @@ namespace g4 {
 // runtime's driver entry point, so libg4ring.so has no link-time libcuda dep.
 using PFN_write64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
 using PFN_wait64 = CUresult (*)(CUstream, CUdeviceptr, cuuint64_t, unsigned int);
+using PFN_addr_range = CUresult (*)(CUdeviceptr*, size_t*, CUdeviceptr);
 
 static g4_status driver_fn(const char* name, void** fn) {
     cudaDriverEntryPointQueryResult q{};
@@ -62,29 +66,73 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ RedParam
 
 extern "C" {
 
-g4_status g4_ipc_export(void* dev_ptr, void* handle_out) {
+// Exported pointers may lie inside a larger allocation (torch's caching
+// allocator): the handle names the allocation, `offset` locates the pointer in it.
+g4_status g4_ipc_export(void* dev_ptr, void* handle_out, int64_t* offset_out) {
     using namespace g4;
-    if (!dev_ptr || !handle_out) return fail(G4_ERR_CONTRACT, "ipc_export: null pointer");
+    if (!dev_ptr || !handle_out || !offset_out) return fail(G4_ERR_CONTRACT, "ipc_export: null pointer");
     static_assert(sizeof(cudaIpcMemHandle_t) == G4_IPC_HANDLE_BYTES, "IPC handle size");
+    static PFN_addr_range range = nullptr;
+    if (!range) G4_TRY(driver_fn("cuMemGetAddressRange", reinterpret_cast<void**>(&range)));
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    CUresult r = range(&base, &size, (CUdeviceptr)dev_ptr);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuMemGetAddressRange failed (CUresult %d)", (int)r);
+        return G4_ERR_CUDA;
+    }
     cudaIpcMemHandle_t h;
-    G4_CUDA(cudaIpcGetMemHandle(&h, dev_ptr));
+    G4_CUDA(cudaIpcGetMemHandle(&h, reinterpret_cast<void*>(base)));
     std::memcpy(handle_out, &h, sizeof(h));
+    *offset_out = (int64_t)((CUdeviceptr)dev_ptr - base);
     return G4_OK;
 }
 
-g4_status g4_ipc_import(const void* handle, void** dev_ptr_out) {
+// Imports are reference counted per allocation: a process may map a given
+// allocation only once, while several exported tensors can share it.
+namespace {
+struct Mapping {
+    void* base;
+    int refs;
+};
+std::mutex g_ipc_mu;
+std::map<std::string, Mapping> g_by_handle;     // handle bytes -> mapping
+std::map<uintptr_t, std::string> g_ptr_handle;  // returned pointer -> handle bytes
+}  // namespace
+
+g4_status g4_ipc_import(const void* handle, int64_t offset, void** dev_ptr_out) {
     using namespace g4;
-    if (!handle || !dev_ptr_out) return fail(G4_ERR_CONTRACT, "ipc_import: null pointer");
-    cudaIpcMemHandle_t h;
-    std::memcpy(&h, handle, sizeof(h));
-    G4_CUDA(cudaIpcOpenMemHandle(dev_ptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    if (!handle || !dev_ptr_out || offset < 0) return fail(G4_ERR_CONTRACT, "ipc_import: bad arguments");
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    const std::string key(static_cast<const char*>(handle), G4_IPC_HANDLE_BYTES);
+    auto it = g_by_handle.find(key);
+    if (it == g_by_handle.end()) {
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof(h));
+        void* base = nullptr;
+        G4_CUDA(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+        it = g_by_handle.emplace(key, Mapping{base, 0}).first;
+    }
+    it->second.refs += 1;
+    void* p = static_cast<char*>(it->second.base) + offset;
+    g_ptr_handle[reinterpret_cast<uintptr_t>(p)] = key;
+    *dev_ptr_out = p;
     return G4_OK;
 }
 
 g4_status g4_ipc_close(void* dev_ptr) {
     using namespace g4;
     if (!dev_ptr) return G4_OK;
-    G4_CUDA(cudaIpcCloseMemHandle(dev_ptr));
+    std::lock_guard<std::mutex> lk(g_ipc_mu);
+    auto pit = g_ptr_handle.find(reinterpret_cast<uintptr_t>(dev_ptr));
+    if (pit == g_ptr_handle.end()) return fail(G4_ERR_CONTRACT, "ipc_close: pointer was not imported");
+    auto it = g_by_handle.find(pit->second);
+    g_ptr_handle.erase(pit);
+    if (it != g_by_handle.end() && --it->second.refs == 0) {
+        void* base = it->second.base;
+        g_by_handle.erase(it);
+        G4_CUDA(cudaIpcCloseMemHandle(base));
+    }
     return G4_OK;
 }
 

@@ -1,0 +1,608 @@
+"""Ring driver on B200s -- the replacement of ``ringacc.engine``
+(/root/reference/pkg/src/ringacc/engine.py) for device-resident payloads.
+
+One process per GPU.  ``torch.distributed`` (gloo) is the control plane only:
+rendezvous, communicator splits, the one-time exchange of CUDA IPC handles,
+barriers.  The data path never touches the host:
+
+* payload transfers are copy-engine peer copies (``g4_copy_async``) straight
+  into the right neighbour's receive slot over NVLink/NVSwitch (no SM cycles);
+* ordering is carried by 64-bit sequence flags in the receiver's / sender's
+  memory, written with ``cuStreamWriteValue64`` and awaited with
+  ``cuStreamWaitValue64`` (``g4_flag_write`` / ``g4_flag_wait``): no host round
+  trip per step, and the K1 pass over the payload received at step j runs on
+  the compute stream while the comm stream forwards that same payload (and
+  receives the next one);
+* the schedule of every round is the host-logic plan of ``schedule.py``;
+* the end-of-run cross-sub-ring reduction sums matching slices in canonical
+  rank order with a kernel that reads the peers' slices over NVLink
+  (``g4_reduce_sum``), bitwise equal to the reference's ``reduce_sum``.
+
+Several ranks may share one GPU (the same code path; peer copies become local
+copies), which is how the multi-rank path is tested on a single B200.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+import socket
+import time
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from . import schedule as S
+from .errors import ConfigError, ContractViolation, DeadlockError
+from .schedule import LaneRing, RingTopology, lane_ring_id  # noqa: F401  (re-exported API)
+from .tensor import (CombinedIndexSpace, GtSlice, Origin, _dtype_code, make_partition,
+                     staged_shape)
+
+VALUE_MODES = ("float", "integer")
+_MODE_CODE = {"float": _lib.G4_MODE_FLOAT, "integer": _lib.G4_MODE_INTEGER}
+
+
+@dataclass
+class ExperimentConfig:
+    """Run shape -- the fields of ringacc.config.ExperimentConfig (config.py:46-83)
+    that concern the hot path, plus the B200 extensions."""
+
+    n_k: int
+    n_w: int
+    world_size: int
+    subring_size: int
+    lanes: int
+    measurements: int
+    seed: int = 0
+    value_mode: str = "float"
+    direction: str = "forward"
+    timeout_s: float = 30.0
+    instrument: bool = True
+    # B200 extensions
+    planes: int | None = None      # exchange planes K3 in [0, planes); None = all N (reference)
+    batch: int = 1                 # measurements per lane carried by one ring message / K1 pass
+    dtype: str = "c128"            # "c128" (reference) or "c64"
+    gather: bool = True            # assemble the full tensor on world rank 0
+    # test hooks (never part of a user config, as in the reference)
+    ring_steps_override: int | None = None
+    fault: str | None = None
+
+    @property
+    def space_size(self) -> int:
+        return self.n_k * self.n_w
+
+    @property
+    def num_planes(self) -> int:
+        return self.space_size if self.planes is None else self.planes
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+def validate_config(cfg: ExperimentConfig) -> None:
+    """config.py:156-185 semantics (ConfigError), plus the extensions."""
+    for name in ("n_k", "n_w", "world_size", "subring_size", "lanes", "measurements", "batch"):
+        v = getattr(cfg, name)
+        if not isinstance(v, int) or v < 1:
+            raise ConfigError(f"{name} must be an integer >= 1, got {v!r}")
+    if not isinstance(cfg.seed, int) or cfg.seed < 0:
+        raise ConfigError(f"seed must be a non-negative integer, got {cfg.seed!r}")
+    if cfg.world_size % cfg.subring_size != 0:
+        raise ConfigError(f"subring_size {cfg.subring_size} does not divide world_size {cfg.world_size}")
+    if not (1 <= cfg.num_planes <= cfg.space_size):
+        raise ConfigError(f"planes must be in [1, {cfg.space_size}], got {cfg.num_planes}")
+    if cfg.subring_size > cfg.num_planes:
+        raise ConfigError(f"subring_size {cfg.subring_size} exceeds the {cfg.num_planes} exchange planes: "
+                          "some rank would own an empty slice")
+    if cfg.lanes >= S.MAX_LANES:
+        raise ConfigError(f"lanes must be < {S.MAX_LANES} (tag stride), got {cfg.lanes}")
+    if cfg.value_mode not in VALUE_MODES:
+        raise ConfigError(f"value_mode must be one of {VALUE_MODES}, got {cfg.value_mode!r}")
+    if cfg.direction not in ("forward", "alternate"):
+        raise ConfigError(f"direction must be forward or alternate, got {cfg.direction!r}")
+    if cfg.dtype not in ("c128", "c64"):
+        raise ConfigError(f"dtype must be c128 or c64, got {cfg.dtype!r}")
+    if cfg.timeout_s <= 0:
+        raise ConfigError("timeout_s must be positive")
+
+
+# ---------------------------------------------------------------------------
+# control plane
+
+class Control:
+    """A group of ranks for control messages (torch.distributed, gloo)."""
+
+    def __init__(self, group=None, ranks: tuple[int, ...] | None = None):
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.world_ranks = ranks if ranks is not None else tuple(range(dist.get_world_size()))
+            self.rank = self.world_ranks.index(dist.get_rank())
+        else:
+            self.world_ranks = (0,)
+            self.rank = 0
+        self.size = len(self.world_ranks)
+
+    def allgather(self, obj) -> list:
+        if self.size == 1:
+            return [obj]
+        out = [None] * self.size
+        dist.all_gather_object(out, obj, group=self.group)
+        return out
+
+    def barrier(self) -> None:
+        if self.size > 1:
+            dist.barrier(group=self.group)
+
+    def split(self, color: int, key: int) -> "Control":
+        """Communicator split (transport/base.py:92-124): groups by color, ranked
+        by (key, parent rank).  Collective over all ranks of this group."""
+        entries = self.allgather((color, key, self.rank))
+        groups: dict[int, list[tuple[int, int]]] = {}
+        for c, k, r in entries:
+            groups.setdefault(c, []).append((k, r))
+        mine = None
+        for c in sorted(groups):
+            members = tuple(self.world_ranks[r] for _, r in sorted(groups[c]))
+            g = dist.new_group(list(members)) if self.size > 1 else None  # every rank creates every group
+            if c == color:
+                mine = (g, members)
+        return Control(*mine)
+
+
+def build_subrings(world: Control, subring_size: int) -> Control:
+    """Consecutive ranks form each sub-ring: color r // S, key r % S (engine.py:86-92)."""
+    if world.size % subring_size != 0:
+        raise ConfigError(f"subring size {subring_size} does not divide world size {world.size}")
+    return world.split(world.rank // subring_size, world.rank % subring_size)
+
+
+# ---------------------------------------------------------------------------
+# peer memory helpers
+
+def export_ptr(ptr: int) -> tuple[bytes, int]:
+    lib = _lib.load()
+    h = ctypes.create_string_buffer(_lib.G4_IPC_HANDLE_BYTES)
+    off = ctypes.c_int64()
+    _lib.check(lib.g4_ipc_export(ptr, h, ctypes.byref(off)), "ipc_export")
+    return h.raw, off.value
+
+
+class PeerMap:
+    """Imported peer pointers of this process (closed together)."""
+
+    def __init__(self):
+        self.ptrs: list[int] = []
+
+    def open(self, handle: bytes, offset: int, local_ptr: int | None = None) -> int:
+        if local_ptr is not None:  # our own buffer: no IPC needed
+            return local_ptr
+        lib = _lib.load()
+        out = ctypes.c_void_p()
+        _lib.check(lib.g4_ipc_import(handle, offset, ctypes.byref(out)), "ipc_import")
+        self.ptrs.append(out.value)
+        return out.value
+
+    def close(self) -> None:
+        lib = _lib.load()
+        for p in self.ptrs:
+            lib.g4_ipc_close(p)
+        self.ptrs = []
+
+
+def reduce_sum(ctl: Control, data: torch.Tensor, root: int = 0) -> None:
+    """Entrywise sum of the members' `data` into root's `data`, in canonical rank
+    order 0, 1, 2, ... (transport/base.py:126-149), reading peers' tensors over
+    NVLink with one kernel.  Collective over `ctl`."""
+    if ctl.size == 1:
+        return
+    dev = data.device
+    torch.cuda.current_stream(dev).synchronize()
+    me = (export_ptr(data.data_ptr()), tuple(data.shape), str(data.dtype))
+    allm = ctl.allgather(me)
+    if any(m[1:] != me[1:] for m in allm):
+        raise ContractViolation("reduce_sum shape/dtype mismatch across ranks")
+    if ctl.rank == root:
+        pm = PeerMap()
+        try:
+            srcs = [pm.open(h, off, data.data_ptr() if r == ctl.rank else None)
+                    for r, ((h, off), _, _) in enumerate(allm)]
+            lib = _lib.load()
+            stream = torch.cuda.current_stream(dev)
+            _lib.check(lib.g4_reduce_sum(data.data_ptr(), _lib.ptr_array(srcs), len(srcs), data.numel(),
+                                         _dtype_code(data.dtype), stream.cuda_stream), "reduce_sum")
+            stream.synchronize()
+        finally:
+            pm.close()
+    ctl.barrier()
+
+
+# ---------------------------------------------------------------------------
+# the per-rank ring executor
+
+@dataclass
+class LaneCounters:
+    """Per-(rank, lane) counters (instrument.py:14-33 semantics)."""
+
+    envelopes_sent: int = 0       # payloads (measurements) forwarded to the next rank
+    envelopes_received: int = 0
+    accumulations_applied: int = 0
+    messages_sent: int = 0        # ring messages (one per step; carries `batch` payloads)
+    bytes_sent: int = 0
+
+    def to_dict(self) -> dict:
+        return asdict(self)
+
+
+class RingEngine:
+    """Everything one rank of one sub-ring does on its GPU."""
+
+    def __init__(self, cfg: ExperimentConfig, sub: Control, world_rank: int, device: torch.device):
+        self.cfg = cfg
+        self.sub = sub
+        self.world_rank = world_rank
+        self.device = device
+        self.pos = sub.rank
+        self.subring = world_rank // cfg.subring_size
+        self.topo = RingTopology(cfg.world_size, cfg.subring_size, cfg.lanes, cfg.direction)
+        self.space = CombinedIndexSpace(cfg.n_k, cfg.n_w)
+        n = self.space.size
+        self.lo, self.hi = make_partition(cfg.num_planes, cfg.subring_size).ranges[self.pos]
+        self.dtype = torch.complex128 if cfg.dtype == "c128" else torch.complex64
+        self.code = _dtype_code(self.dtype)
+        self.slice = GtSlice.zeros(self.space, self.lo, self.hi, device=device, dtype=self.dtype)
+        self.channels = S.make_channels(self.topo, self.pos)
+        self.lib = _lib.load()
+        # per channel: 3 buffers (GEN, R0, R1) x batch x lanes staged payloads
+        self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n), dtype=self.dtype,
+                                 device=device) for c in self.channels]
+        self.payload_bytes = int(np.prod(staged_shape(n))) * self.bufs[0].element_size()
+        self.flags = torch.zeros(len(self.channels) * S.FLAGS_PER_CHANNEL, dtype=torch.int64, device=device)
+        self.compute = torch.cuda.Stream(device)
+        self.comm = [torch.cuda.Stream(device) for _ in self.channels]
+        self.events: dict[str, torch.cuda.Event] = {}
+        self.counters = {t: LaneCounters() for t in range(cfg.lanes)}
+        self.origins = {t: [] for t in range(cfg.lanes)}
+        self.meas_count = 0
+        self.peers = PeerMap()
+        self._connect()
+
+    # -- setup --------------------------------------------------------------
+    def _connect(self) -> None:
+        mine = {"flags": export_ptr(self.flags.data_ptr()),
+                "bufs": [export_ptr(b.data_ptr()) for b in self.bufs],
+                "lanes": [c.lanes for c in self.channels]}
+        torch.cuda.synchronize(self.device)
+        everyone = self.sub.allgather(mine)
+        self.peer_flags: dict[int, int] = {}
+        self.peer_bufs: dict[tuple[int, int], int] = {}
+        for c in self.channels:
+            for p in (c.send_to, c.recv_from):
+                local = p == self.pos
+                if p not in self.peer_flags:
+                    h, off = everyone[p]["flags"]
+                    self.peer_flags[p] = self.peers.open(h, off, self.flags.data_ptr() if local else None)
+            if everyone[c.send_to]["lanes"][c.index] != c.lanes:
+                raise ContractViolation("neighbouring ranks disagree on lane grouping")
+            h, off = everyone[c.send_to]["bufs"][c.index]
+            self.peer_bufs[(c.send_to, c.index)] = self.peers.open(
+                h, off, self.bufs[c.index].data_ptr() if c.send_to == self.pos else None)
+
+    def close(self) -> None:
+        torch.cuda.synchronize(self.device)
+        self.sub.barrier()
+        self.peers.close()
+
+    # -- helpers --------------------------------------------------------------
+    def _stream(self, name: str) -> torch.cuda.Stream:
+        return self.compute if name == S.COMPUTE else self.comm[int(name[4:])]
+
+    def _buf_ptr(self, ci: int, buf: int, i: int = 0) -> int:
+        return self.bufs[ci][buf, i].data_ptr()
+
+    def _nb(self, m: int) -> int:
+        """Measurements per lane in round m (the last round may be partial)."""
+        return min(self.cfg.batch, self.cfg.measurements - m * self.cfg.batch)
+
+    def _flag_off(self, ci: int, flag: int) -> int:
+        return (ci * S.FLAGS_PER_CHANNEL + flag) * 8
+
+    # -- one round ------------------------------------------------------------
+    def enqueue_round(self, m: int) -> None:
+        cfg = self.cfg
+        nb = self._nb(m)
+        fault = cfg.fault == "skip-send" and self.world_rank == 0 and m == 0
+        ops = S.round_schedule(self.topo, self.pos, self.channels, m, cfg.ring_steps_override, fault)
+        lib = self.lib
+        s = cfg.subring_size
+        for op in ops:
+            kind = op[0]
+            if kind == "gen":
+                ptrs, wr, lanes, meas = [], [], [], []
+                for c in self.channels:
+                    for b in range(nb):
+                        for li, t in enumerate(c.lanes):
+                            ptrs.append(self._buf_ptr(c.index, S.GEN, b * len(c.lanes) + li))
+                            wr.append(self.world_rank)
+                            lanes.append(t)
+                            meas.append(m * cfg.batch + b)
+                _lib.check(lib.g4_generate(_lib.ptr_array(ptrs), None, None, len(ptrs),
+                                           cfg.seed & 0xFFFFFFFFFFFFFFFF, _lib.i64_array(wr),
+                                           _lib.i64_array(lanes), _lib.i64_array(meas), self.space.size,
+                                           _MODE_CODE[cfg.value_mode], self.code, self.compute.cuda_stream),
+                           "generate")
+            elif kind == "acc":
+                ptrs = []
+                for ci, buf in op[1]:
+                    c = self.channels[ci]
+                    ptrs += [self._buf_ptr(ci, buf, i) for i in range(nb * len(c.lanes))]
+                    for li, t in enumerate(c.lanes):
+                        self.counters[t].accumulations_applied += nb
+                        if buf != S.GEN:
+                            self.counters[t].envelopes_received += nb
+                        if cfg.instrument:
+                            if buf == S.GEN:
+                                bp = self.pos
+                            else:
+                                bp = S.birth_position(self.pos, op[2][2], s, c.backward)
+                            self.origins[t] += [(self.subring, bp, t, m * cfg.batch + b,
+                                                 self.subring * s + bp) for b in range(nb)]
+                _lib.check(lib.g4_accumulate_staged(self.slice.data.data_ptr(), self.lo, self.hi,
+                                                    self.space.size, _lib.ptr_array(ptrs), len(ptrs),
+                                                    self.code, _lib.G4_CHANNEL_EQ1,
+                                                    self.compute.cuda_stream), "accumulate")
+                self.slice.meas_count += len(ptrs)
+                self.meas_count += len(ptrs)
+            elif kind == "wait":
+                _, st, ci, flag, value = op
+                _lib.check(lib.g4_flag_wait(self.flags.data_ptr() + self._flag_off(ci, flag), value,
+                                            self._stream(st).cuda_stream), "flag_wait")
+            elif kind == "write":
+                _, st, peer, ci, flag, value = op
+                _lib.check(lib.g4_flag_write(self.peer_flags[peer] + self._flag_off(ci, flag), value,
+                                             self._stream(st).cuda_stream), "flag_write")
+            elif kind == "copy":
+                _, st, ci, src, peer, dst = op
+                c = self.channels[ci]
+                nbytes = nb * len(c.lanes) * self.payload_bytes
+                dst_ptr = self.peer_bufs[(peer, ci)] + dst * self.bufs[ci][0].numel() * self.bufs[ci].element_size()
+                _lib.check(lib.g4_copy_async(dst_ptr, self._buf_ptr(ci, src), nbytes,
+                                             self._stream(st).cuda_stream), "copy_async")
+                for t in c.lanes:
+                    self.counters[t].envelopes_sent += nb
+                    self.counters[t].messages_sent += 1
+                    self.counters[t].bytes_sent += nbytes // len(c.lanes)
+            elif kind == "record":
+                ev = self.events.setdefault(op[2], torch.cuda.Event())
+                ev.record(self._stream(op[1]))
+            elif kind == "wait_event":
+                ev = self.events.get(op[2])
+                if ev is not None:
+                    self._stream(op[1]).wait_event(ev)
+            else:  # pragma: no cover
+                raise AssertionError(kind)
+
+    def rounds(self) -> int:
+        return -(-self.cfg.measurements // self.cfg.batch)
+
+    def wait_idle(self, timeout_s: float) -> None:
+        """Host watchdog: all streams drained within the timeout, else a
+        DeadlockError naming the stalled (rank, lane, measurement, step)."""
+        done = torch.cuda.Event()
+        for st in [self.compute] + self.comm:
+            done.record(st)
+            t0 = time.monotonic()
+            while not done.query():
+                if time.monotonic() - t0 > timeout_s:
+                    self._raise_deadlock()
+                time.sleep(0.0005)
+
+    def _raise_deadlock(self):
+        vals = torch.zeros_like(self.flags, device="cpu")
+        side = torch.cuda.Stream(self.device)
+        with torch.cuda.stream(side):
+            vals.copy_(self.flags, non_blocking=True)
+        side.synchronize()
+        s = self.cfg.subring_size
+        for c in self.channels:
+            landed = int(vals[c.index * S.FLAGS_PER_CHANNEL + S.DATA])
+            k = max(landed + 1, S.FIRST_TRANSFER)
+            m, j = divmod(k - S.FIRST_TRANSFER, max(s - 1, 1))
+            # unblock the streams so the process can tear down, then report
+            with torch.cuda.stream(side):
+                self.flags.fill_(1 << 62)
+            side.synchronize()
+            raise DeadlockError(f"rank {self.world_rank} lane {c.lanes[0]} stalled at measurement "
+                                f"{m * self.cfg.batch} step {j}: no payload from rank "
+                                f"{self.subring * s + c.recv_from}", rank=self.world_rank,
+                                lane=c.lanes[0], step=j)
+        raise DeadlockError(f"rank {self.world_rank} stalled", rank=self.world_rank)
+
+
+# ---------------------------------------------------------------------------
+# experiment driver
+
+@dataclass
+class ExperimentReport:
+    """engine.py:187-220 fields that apply to the device engine."""
+
+    config: dict
+    tensor: np.ndarray | None
+    meas_counts: dict[int, int]
+    lane_counters: dict[tuple[int, int], dict]
+    lane_meta: dict[tuple[int, int], dict]
+    memory_peaks: dict[int, int]
+    slices: dict[int, tuple[int, int]]
+    elapsed_s: float
+    clock: str = "cuda-event"
+    round_ms: dict[int, list[float]] = field(default_factory=dict)
+
+    def to_json_dict(self) -> dict:
+        return {"config": self.config, "clock": self.clock, "elapsed_s": self.elapsed_s,
+                "meas_counts": {str(r): v for r, v in sorted(self.meas_counts.items())},
+                "slices": {str(r): list(v) for r, v in sorted(self.slices.items())},
+                "counters": {f"{r}/{t}": c for (r, t), c in sorted(self.lane_counters.items())},
+                "lane_meta": {f"{r}/{t}": m for (r, t), m in sorted(self.lane_meta.items())},
+                "memory_peaks": {str(r): p for r, p in sorted(self.memory_peaks.items())}}
+
+
+def device_for_rank(rank: int) -> torch.device:
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    return torch.device("cuda", local % max(torch.cuda.device_count(), 1))
+
+
+def rank_main(cfg: ExperimentConfig, world: Control | None = None) -> ExperimentReport | None:
+    """Everything one rank does (engine.py:241-297); the report on world rank 0."""
+    validate_config(cfg)
+    world = world or Control()
+    if world.size != cfg.world_size:
+        raise ConfigError(f"world_size {cfg.world_size} but {world.size} ranks are running")
+    r = world.rank
+    device = device_for_rank(r)
+    torch.cuda.set_device(device)
+    torch.cuda.reset_peak_memory_stats(device)
+    sub = build_subrings(world, cfg.subring_size)
+    pos_group = world.split(r % cfg.subring_size, r // cfg.subring_size)  # same position across sub-rings
+    eng = RingEngine(cfg, sub, r, device)
+    world.barrier()
+    t0 = time.monotonic()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    start.record(eng.compute)
+    error = None
+    try:
+        for m in range(eng.rounds()):
+            eng.enqueue_round(m)
+        end.record(eng.compute)
+        eng.wait_idle(cfg.timeout_s)
+    except DeadlockError as exc:
+        error = exc
+    if error is not None:
+        raise error
+    elapsed = time.monotonic() - t0
+    gpu_ms = start.elapsed_time(end)
+    torch.cuda.synchronize(device)
+    world.barrier()
+
+    reduce_sum(pos_group, eng.slice.data, root=0)
+
+    tensor = None
+    if cfg.gather:
+        tensor = _gather_full(world, eng, cfg)
+    blob = {"rank": r, "meas_count": eng.meas_count, "slice": [eng.lo, eng.hi],
+            "counters": {t: c.to_dict() for t, c in eng.counters.items()},
+            "origins": {t: eng.origins[t] for t in eng.origins},
+            "peak": int(torch.cuda.max_memory_allocated(device)), "gpu_ms": gpu_ms}
+    blobs = world.allgather(json.dumps(blob))
+    eng.close()
+    if r != 0:
+        return None
+    meas, slices, peaks, counters, meta, rms = {}, {}, {}, {}, {}, {}
+    for b in map(json.loads, blobs):
+        rr = b["rank"]
+        meas[rr] = b["meas_count"]
+        slices[rr] = tuple(b["slice"])
+        peaks[rr] = b["peak"]
+        rms[rr] = [b["gpu_ms"]]
+        for t, c in b["counters"].items():
+            counters[(rr, int(t))] = c
+            meta[(rr, int(t))] = {"lane": int(t), "allocations": 3, "ring_phase_allocations": 0,
+                                  "isolation_violations": 0,
+                                  "origins": [tuple(o) for o in b["origins"][t]]}
+    return ExperimentReport(config=cfg.to_dict(), tensor=tensor, meas_counts=meas, lane_counters=counters,
+                            lane_meta=meta, memory_peaks=peaks, slices=slices, elapsed_s=elapsed,
+                            round_ms=rms)
+
+
+def _gather_full(world: Control, eng: RingEngine, cfg: ExperimentConfig) -> np.ndarray | None:
+    """World rank 0 assembles the reduced tensor from sub-ring 0's slices (engine.py:287-297)."""
+    s = cfg.subring_size
+    torch.cuda.synchronize(eng.device)
+    info = world.allgather((export_ptr(eng.slice.data.data_ptr()), eng.lo, eng.hi))
+    out = None
+    if world.rank == 0:
+        n = eng.space.size
+        full = torch.empty((cfg.num_planes, n, n), dtype=eng.dtype, device=eng.device)
+        pm = PeerMap()
+        try:
+            for q in range(s):
+                (h, off), lo, hi = info[q]
+                ptr = pm.open(h, off, eng.slice.data.data_ptr() if q == 0 else None)
+                nbytes = (hi - lo) * n * n * full.element_size()
+                _lib.check(eng.lib.g4_copy_async(full[lo:hi].data_ptr(), ptr, nbytes,
+                                                 torch.cuda.current_stream(eng.device).cuda_stream), "gather")
+            torch.cuda.synchronize(eng.device)
+        finally:
+            pm.close()
+        out = full.cpu().numpy()
+    world.barrier()
+    return out
+
+
+# ---------------------------------------------------------------------------
+# launcher: one OS process per rank (the role of transport/tcp.py's launcher)
+
+def _free_port() -> int:
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank: int, cfg_dict: dict, port: int, q) -> None:
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(cfg_dict["world_size"]), LOCAL_RANK=str(rank))
+    try:
+        dist.init_process_group("gloo", rank=rank, world_size=cfg_dict["world_size"])
+        rep = rank_main(ExperimentConfig(**cfg_dict))
+        q.put((rank, "ok", rep))
+    except Exception as exc:  # reported to the launcher
+        q.put((rank, "error", exc))
+    finally:
+        if dist.is_initialized():
+            try:
+                dist.destroy_process_group()
+            except Exception:
+                pass
+
+
+def run_experiment(cfg: ExperimentConfig) -> ExperimentReport:
+    """Run a whole experiment (engine.py:323-335).  Inside an initialised
+    torch.distributed world every rank calls this; otherwise one process per
+    rank is spawned on this node (ranks share GPUs round-robin)."""
+    validate_config(cfg)
+    if dist.is_available() and dist.is_initialized():
+        return rank_main(cfg)
+    if cfg.world_size == 1:
+        return rank_main(cfg)
+    import torch.multiprocessing as tmp
+    ctx = tmp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, cfg.to_dict(), port, q), daemon=True)
+             for r in range(cfg.world_size)]
+    for p in procs:
+        p.start()
+    results, error = {}, None
+    deadline = time.monotonic() + max(120.0, 4 * cfg.timeout_s)
+    while len(results) < cfg.world_size and time.monotonic() < deadline:
+        try:
+            rank, status, payload = q.get(timeout=1.0)
+        except Exception:
+            if any(p.exitcode not in (None, 0) for p in procs) and error is None:
+                error = RuntimeError("a rank process died")
+                break
+            continue
+        results[rank] = (status, payload)
+        if status == "error":
+            error = payload
+            break
+    for p in procs:
+        p.join(timeout=5 if error is None else 0.5)
+        if p.is_alive():
+            p.kill()
+    if error is not None:
+        raise error
+    if len(results) < cfg.world_size:
+        raise DeadlockError("experiment did not finish before the launcher deadline")
+    return results[0][1]

@@ -1,0 +1,116 @@
+"""The ring driver on the GPU: several rank processes (sharing the one B200 of
+the test box, or one per GPU) connected through CUDA IPC peer memory, copy-
+engine transfers and stream flags.  Compared with the oracle and with the
+reference engine's golden outputs.  GPU only.
+
+Tolerances: integer mode bitwise (any accumulation order); float mode 1e-10
+relative (north_star: the ring reorders walkers).
+"""
+import numpy as np
+import pytest
+
+from oracle import oracle as O
+from paper_2105_00027_b200 import engine as E
+from paper_2105_00027_b200.errors import ConfigError, DeadlockError
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg(**kw):
+    base = dict(n_k=2, n_w=4, world_size=1, subring_size=1, lanes=1, measurements=2, seed=11,
+                value_mode="integer", timeout_s=20.0)
+    base.update(kw)
+    return E.ExperimentConfig(**base)
+
+
+def oracle_of(c):
+    return O.oracle_full(c.seed, c.space_size, c.world_size // c.subring_size, c.subring_size, c.lanes,
+                         c.measurements, c.value_mode, 0, c.num_planes)
+
+
+def check(c, rep):
+    ref = oracle_of(c)
+    if c.value_mode == "integer":
+        assert np.array_equal(rep.tensor, ref)
+    else:
+        np.testing.assert_allclose(rep.tensor, ref, rtol=1e-10, atol=1e-10 * np.abs(ref).max())
+    s, k, m = c.subring_size, c.lanes, c.measurements
+    steps = s - 1 if c.ring_steps_override is None else c.ring_steps_override
+    for r in range(c.world_size):
+        for t in range(k):
+            cnt = rep.lane_counters[(r, t)]
+            assert cnt["envelopes_sent"] == steps * m and cnt["envelopes_received"] == steps * m
+            assert cnt["accumulations_applied"] == (steps + 1) * m
+            origins = rep.lane_meta[(r, t)]["origins"]
+            assert len(origins) == len(set(origins)) == (steps + 1) * m
+            assert all(o[2] == t and o[0] == r // s for o in origins)
+        assert rep.meas_counts[r] == (steps + 1) * m * k
+
+
+@pytest.mark.parametrize("mode", ["integer", "float"])
+def test_single_rank_is_serial_oracle(mode):
+    c = cfg(value_mode=mode, measurements=5, lanes=2)
+    check(c, E.run_experiment(c))
+
+
+@pytest.mark.parametrize("kw", [
+    dict(world_size=2, subring_size=2),
+    dict(world_size=4, subring_size=4, lanes=2, measurements=3),
+    dict(world_size=4, subring_size=2, lanes=1, measurements=2),          # 2 sub-rings + reduce
+    dict(world_size=3, subring_size=3, lanes=3, direction="alternate", n_w=3),
+    dict(world_size=4, subring_size=4, lanes=2, batch=2, measurements=5),  # batched rounds, partial last
+    dict(world_size=4, subring_size=2, lanes=2, value_mode="float", n_k=8, n_w=16, planes=64),
+])
+def test_multi_rank_ring_matches_oracle(kw):
+    c = cfg(**kw)
+    check(c, E.run_experiment(c))
+
+
+def test_reference_engine_golden(golden):
+    """Same configs as the reference run_experiment golden outputs (engine.npz)."""
+    e = golden("engine.npz")
+    for i in (0, 2):
+        nk, nw, world, s, lanes, m, seed = (int(x) for x in e[f"c{i}_cfg"])
+        for mode in ("integer", "float"):
+            c = cfg(n_k=nk, n_w=nw, world_size=world, subring_size=s, lanes=lanes, measurements=m,
+                    seed=seed, value_mode=mode)
+            rep = E.run_experiment(c)
+            want = e[f"c{i}_{mode}_tensor"]
+            if mode == "integer":
+                assert np.array_equal(rep.tensor, want)
+            else:
+                np.testing.assert_allclose(rep.tensor, want, rtol=1e-10, atol=1e-12)
+            assert [rep.slices[r] for r in range(world)] == [tuple(x) for x in e[f"c{i}_{mode}_slices"]]
+
+
+def test_c64_ring_within_tolerance():
+    c = cfg(world_size=2, subring_size=2, lanes=1, measurements=3, value_mode="float", dtype="c64",
+            n_k=4, n_w=16)
+    rep = E.run_experiment(c)
+    ref = oracle_of(c)
+    assert O.compare(ref, rep.tensor.astype(np.complex128))["l2_real"] < 1e-5
+
+
+def test_short_ring_negative_control():
+    c = cfg(world_size=3, subring_size=3, n_w=3, ring_steps_override=1)
+    rep = E.run_experiment(c)
+    assert rep.lane_counters[(0, 0)]["envelopes_sent"] == 1 * 2
+    assert rep.meas_counts[0] == 2 * 2
+    assert not np.array_equal(rep.tensor, oracle_of(c))
+
+
+def test_skipped_send_deadlocks_with_diagnostic():
+    c = cfg(world_size=2, subring_size=2, measurements=1, fault="skip-send", timeout_s=3.0)
+    with pytest.raises(DeadlockError) as err:
+        E.run_experiment(c)
+    msg = str(err.value)
+    assert "rank 1" in msg and "lane 0" in msg and "step 0" in msg
+
+
+def test_config_errors():
+    with pytest.raises(ConfigError):
+        E.validate_config(cfg(world_size=6, subring_size=4))
+    with pytest.raises(ConfigError):
+        E.validate_config(cfg(world_size=16, subring_size=16))  # more ranks than planes
+    with pytest.raises(ConfigError):
+        E.validate_config(cfg(lanes=1000))
