@@ -267,6 +267,8 @@ class RingEngine:
         self.origins = {t: [] for t in range(cfg.lanes)}
         self.meas_count = 0
         self.peers = PeerMap()
+        self.kernel_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] | None = None
+        self.next_round = 0
         self._connect()
 
     # -- setup --------------------------------------------------------------
@@ -310,11 +312,22 @@ class RingEngine:
         return (ci * S.FLAGS_PER_CHANNEL + flag) * 8
 
     # -- one round ------------------------------------------------------------
-    def enqueue_round(self, m: int) -> None:
+    def enqueue_round(self, m: int | None = None, regenerate: bool = True) -> None:
+        """Enqueue the next round (asynchronous).  Rounds must be consecutive:
+        transfer indices (and therefore the flags) are derived from the round
+        number.  `m` defaults to the next round; regenerate=False reuses the
+        payloads already in GEN (benchmarking with resident inputs)."""
+        if m is None:
+            m = self.next_round
+        if m != self.next_round:
+            raise ContractViolation(f"rounds must be consecutive: expected {self.next_round}, got {m}")
+        self.next_round = m + 1
         cfg = self.cfg
-        nb = self._nb(m)
+        nb = max(1, min(self._nb(m), cfg.batch)) if regenerate else cfg.batch
         fault = cfg.fault == "skip-send" and self.world_rank == 0 and m == 0
         ops = S.round_schedule(self.topo, self.pos, self.channels, m, cfg.ring_steps_override, fault)
+        if not regenerate:
+            ops = [op for op in ops if op[0] != "gen"]
         lib = self.lib
         s = cfg.subring_size
         for op in ops:
@@ -349,10 +362,16 @@ class RingEngine:
                                 bp = S.birth_position(self.pos, op[2][2], s, c.backward)
                             self.origins[t] += [(self.subring, bp, t, m * cfg.batch + b,
                                                  self.subring * s + bp) for b in range(nb)]
+                if self.kernel_events is not None:
+                    ev = (torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    ev[0].record(self.compute)
                 _lib.check(lib.g4_accumulate_staged(self.slice.data.data_ptr(), self.lo, self.hi,
                                                     self.space.size, _lib.ptr_array(ptrs), len(ptrs),
                                                     self.code, _lib.G4_CHANNEL_EQ1,
                                                     self.compute.cuda_stream), "accumulate")
+                if self.kernel_events is not None:
+                    ev[1].record(self.compute)
+                    self.kernel_events.append(ev)
                 self.slice.meas_count += len(ptrs)
                 self.meas_count += len(ptrs)
             elif kind == "wait":
@@ -383,6 +402,19 @@ class RingEngine:
                     self._stream(op[1]).wait_event(ev)
             else:  # pragma: no cover
                 raise AssertionError(kind)
+
+    def stage_gen(self, ups: list[torch.Tensor], downs: list[torch.Tensor]) -> None:
+        """Fill the GEN buffers from reference-layout device matrices (K2), in
+        channel order, batch-major -- the walker hand-off of a host-fed run."""
+        ptrs = [self._buf_ptr(c.index, S.GEN, i) for c in self.channels
+                for i in range(self.cfg.batch * len(c.lanes))]
+        if len(ups) != len(ptrs) or len(downs) != len(ptrs):
+            raise ContractViolation(f"expected {len(ptrs)} payloads, got {len(ups)}")
+        code_in = _dtype_code(ups[0].dtype)
+        _lib.check(self.lib.g4_prepare_g(_lib.ptr_array(ptrs), _lib.ptr_array([u.data_ptr() for u in ups]),
+                                         _lib.ptr_array([d.data_ptr() for d in downs]), len(ptrs),
+                                         self.space.size, code_in, self.code, self.compute.cuda_stream),
+                   "prepare_g")
 
     def rounds(self) -> int:
         return -(-self.cfg.measurements // self.cfg.batch)
