@@ -228,6 +228,7 @@ def run_gpu(args):
         return run_ring(args)
 
     lib = _lib.load()
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if args.arith == "fused" else _lib.G4_ARITH_EXACT))
     n_k, n_w, planes, desc = CONFIGS[args.config]
     sp = T.CombinedIndexSpace(n_k, n_w)
     n = sp.size
@@ -273,7 +274,7 @@ def run_gpu(args):
     line = {
         "metric": "G4 updates/s", "value": value, "unit": "updates/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "arith": args.arith,
         "data": "synthetic (reference counter-based generator on device, float mode, seed 0)",
         "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
                    "walkers_per_pass": B, "subring_size": 1, "lanes": 1,
@@ -514,6 +515,8 @@ def main():
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=8, help="walkers per K1 pass (per rank)")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
+    ap.add_argument("--arith", default="exact", choices=["exact", "fused"],
+                    help="exact: reference op order (bitwise); fused: FMA-chained (within 1e-10)")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -38,8 +38,8 @@ extern "C" {
 
 #define G4RING_ABI_VERSION 1
 #define G4_MAX_BATCH 64 /* walkers per accumulate launch (more are chunked) */
-#define G4_HALO_ROWS 32 /* staged-layout halo (see above) */
-#define G4_HALO_COLS 64
+#define G4_HALO_ROWS 40 /* staged-layout halo (see above) */
+#define G4_HALO_COLS 72
 
 typedef enum {
     G4_OK = 0,
@@ -116,6 +116,15 @@ g4_status g4_accumulate_staged(void* g4, int64_t lo, int64_t hi, int32_t n,
  * shared-memory ring, warp-specialised; used for N >= 64).  For A/B
  * measurement and parity tests of both paths (env G4RING_KERNEL). */
 g4_status g4_set_kernel_variant(int32_t variant);
+
+/* Floating-point evaluation of the update (process-wide):
+ *   G4_ARITH_EXACT (default): the reference's op order, rounding every product
+ *     and sum as numpy does -> bitwise equal to ringacc on an FMA host;
+ *   G4_ARITH_FUSED: the same terms as 8 fused multiply-adds chained into the
+ *     accumulator -> within ~1 ulp per update (north_star tolerance 1e-10
+ *     relative), bitwise for integer-valued payloads, ~1.5x fewer FP64 issues. */
+typedef enum { G4_ARITH_EXACT = 0, G4_ARITH_FUSED = 1 } g4_arith_mode;
+g4_status g4_set_arith_mode(int32_t mode);
 
 /* Convenience form taking reference-layout payloads: prepares each batch into
  * `workspace` (>= g4_accumulate_workspace_bytes) then calls g4_accumulate_staged. */

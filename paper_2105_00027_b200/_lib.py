@@ -19,9 +19,10 @@ G4_OK, G4_ERR_CONTRACT, G4_ERR_CONFIG, G4_ERR_TRANSPORT, G4_ERR_DEADLOCK, G4_ERR
 G4_C128, G4_C64 = 0, 1
 G4_MODE_FLOAT, G4_MODE_INTEGER = 0, 1
 G4_CHANNEL_EQ1 = 0
+G4_ARITH_EXACT, G4_ARITH_FUSED = 0, 1
 G4_MAX_BATCH = 64
 G4_IPC_HANDLE_BYTES = 64
-G4_HALO_ROWS, G4_HALO_COLS = 32, 64
+G4_HALO_ROWS, G4_HALO_COLS = 40, 72
 ABI_VERSION = 1
 
 # (name, restype, argtypes) for every symbol include/g4ring.h declares.
@@ -39,6 +40,7 @@ SIGNATURES = {
     "g4_generate": (_i32, [_vpp, _vpp, _vpp, _i32, _u64, _i64p, _i64p, _i64p, _i32, _i32, _i32, _vp]),
     "g4_accumulate_staged": (_i32, [_vp, _i64, _i64, _i32, _vpp, _i32, _i32, _i32, _vp]),
     "g4_set_kernel_variant": (_i32, [_i32]),
+    "g4_set_arith_mode": (_i32, [_i32]),
     "g4_accumulate_workspace_bytes": (_i64, [_i32, _i32, _i32]),
     "g4_accumulate": (_i32, [_vp, _i64, _i64, _i32, _vpp, _vpp, _i32, _i32, _i32, _vp, _i64, _vp]),
     "g4_ipc_export": (_i32, [_vp, _vp, _i64p]),

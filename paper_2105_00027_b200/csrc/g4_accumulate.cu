@@ -69,9 +69,27 @@ __device__ __forceinline__ int wrap(int x, int n) {
     return x;
 }
 
+// G4_ARITH_FUSED: the same two products and sums as 8 FMAs chained into the
+// accumulator (no rounded intermediates): ~1 ulp per update from the reference
+// order, far inside north_star's 1e-10 relative tolerance; integer-valued
+// inputs stay exact.  Each entry is two independent 4-deep FMA chains.
+template <typename R>
+__device__ __forceinline__ void update_fused(Cx<R>& a, const Stg<R>& S, const Stg<R>& D) {
+    R re = fma_rn(S.ur, D.dr, a.re);
+    R im = fma_rn(S.ur, D.di, a.im);
+    re = fma_rn(-S.ui, D.di, re);
+    im = fma_rn(S.ui, D.dr, im);
+    re = fma_rn(S.dr, D.ur, re);
+    im = fma_rn(S.dr, D.ui, im);
+    re = fma_rn(-S.di, D.ui, re);
+    im = fma_rn(S.di, D.ur, im);
+    a.re = re;
+    a.im = im;
+}
+
 // ---------------------------------------------------------------------------
 // v1
-template <typename R, int PP, int DD, int WARPS, int MINB>
+template <typename R, int PP, int DD, int WARPS, int MINB, bool FUSED>
 __global__ void __launch_bounds__(32 * WARPS, MINB)
 k_accumulate(const __grid_constant__ AccParams<R> P) {
     constexpr int NS = PP + DD - 1;  // distinct shifted elements per thread
@@ -143,11 +161,15 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
             for (int d = 0; d < DD; ++d) {
                 const Stg<R>& S = sv[p - d + DD - 1];
                 const Stg<R>& D = dv[d];
-                R p1r, p1i, p2r, p2i;
-                cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);  // u * down[k2][k1]
-                cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);  // d * up[k2][k1]
-                acc[p][d].re = add_rn(acc[p][d].re, add_rn(p1r, p2r));
-                acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
+                if constexpr (FUSED) {
+                    update_fused(acc[p][d], S, D);
+                } else {
+                    R p1r, p1i, p2r, p2i;
+                    cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);  // u * down[k2][k1]
+                    cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);  // d * up[k2][k1]
+                    acc[p][d].re = add_rn(acc[p][d].re, add_rn(p1r, p2r));
+                    acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
+                }
             }
         }
     }
@@ -159,7 +181,7 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
             if (okmask & (1u << (p * DD + d))) st_g4(gb + p * nn + offg[d], acc[p][d]);
 }
 
-template <typename R, int PP, int DD, int WARPS, int MINB>
+template <typename R, int PP, int DD, int WARPS, int MINB, bool FUSED>
 static g4_status launch_v1(const AccParams<R>& prm, cudaStream_t st) {
     const int n = prm.n;
     const int64_t chunks = (prm.hi - prm.lo + PP - 1) / PP;
@@ -167,7 +189,7 @@ static g4_status launch_v1(const AccParams<R>& prm, cudaStream_t st) {
               (unsigned)((n + DD - 1) / DD));
     if (grid.y > 65535u || grid.z > 65535u)
         return fail(G4_ERR_CONTRACT, "accumulate: N too large for the launch grid");
-    k_accumulate<R, PP, DD, WARPS, MINB><<<grid, dim3(32, WARPS), 0, st>>>(prm);
+    k_accumulate<R, PP, DD, WARPS, MINB, FUSED><<<grid, dim3(32, WARPS), 0, st>>>(prm);
     return check_cuda(cudaGetLastError(), "k_accumulate launch");
 }
 
@@ -205,6 +227,18 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+// Plain shared-memory loads the scheduler may move (ordered after the stage's
+// mbarrier wait by that asm's memory clobber).
+__device__ __forceinline__ Stg<double> lds_plain(const Cx<double>* u, const Cx<double>* d) {
+    const double2 a = *reinterpret_cast<const double2*>(u);
+    const double2 b = *reinterpret_cast<const double2*>(d);
+    Stg<double> v;
+    v.ur = a.x;
+    v.ui = a.y;
+    v.dr = b.x;
+    v.di = b.y;
+    return v;
+}
 __device__ __forceinline__ Stg<double> lds_stg(const Cx<double>* u, const Cx<double>* d) {
     Stg<double> v;
     asm volatile("ld.shared.v2.f64 {%0,%1}, [%2];" : "=d"(v.ur), "=d"(v.ui) : "r"(smem_u32(u)));
@@ -213,18 +247,24 @@ __device__ __forceinline__ Stg<double> lds_stg(const Cx<double>* u, const Cx<dou
 }
 
 constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel params)
-constexpr int V2_PP = 4, V2_DD = 4, V2_CW = 4, V2_NST = 3;
-constexpr int V2_DIRLEN = 32 + V2_DD - 1;                 // 35 direct columns
-constexpr int V2_NSH = V2_PP * V2_CW + V2_DD - 1;         // 19 shifted row segments
-constexpr int V2_DIR_ELEMS = V2_DD * V2_DIRLEN;           // per spin
-constexpr int V2_SH_ELEMS = V2_NSH * 32;                  // per spin
-constexpr uint32_t V2_DIR_BYTES = 2 * V2_DIR_ELEMS * 16;  // both spins, complex128
-constexpr uint32_t V2_SH_BYTES = 2 * V2_SH_ELEMS * 16;
-constexpr uint32_t V2_DIR_OFF = 0;
-constexpr uint32_t V2_SH_OFF = (V2_DIR_BYTES + 127) / 128 * 128;
-constexpr uint32_t V2_STAGE_BYTES = (V2_SH_OFF + V2_SH_BYTES + 127) / 128 * 128;
-constexpr size_t V2_SMEM = (size_t)V2_NST * V2_STAGE_BYTES + 2 * V2_NST * sizeof(uint64_t);
-static_assert(V2_NSH <= G4_HALO_ROWS && V2_NSH + 31 < G4_HALO_COLS, "halo too small for the v2 band");
+
+// Geometry of one v2 configuration: PP planes x DD diagonal entries per thread,
+// CW warps stacked along K3 per CTA, NST-stage shared-memory ring.
+template <int PP_, int CW_, int NST_>
+struct V2Geom {
+    static constexpr int PP = PP_, DD = 4, CW = CW_, NST = NST_;
+    static constexpr int DIRLEN = 32 + DD - 1;                    // direct columns
+    static constexpr int NSH = PP * CW + DD - 1;                  // shifted row segments (band height)
+    static constexpr int DIR_ELEMS = DD * DIRLEN;                 // per spin
+    static constexpr int SH_ELEMS = NSH * 32;                     // per spin
+    static constexpr uint32_t DIR_BYTES = 2 * DIR_ELEMS * 16;     // both spins, complex128
+    static constexpr uint32_t SH_BYTES = 2 * SH_ELEMS * 16;
+    static constexpr uint32_t DIR_OFF = 0;
+    static constexpr uint32_t SH_OFF = (DIR_BYTES + 127) / 128 * 128;
+    static constexpr uint32_t STAGE_BYTES = (SH_OFF + SH_BYTES + 127) / 128 * 128;
+    static constexpr size_t SMEM = (size_t)NST * STAGE_BYTES + 2 * NST * sizeof(uint64_t);
+    static_assert(NSH <= G4_HALO_ROWS && NSH + 31 < G4_HALO_COLS, "halo too small for the v2 band");
+};
 
 struct alignas(64) TmaParams {
     CUtensorMap dmap[TMA_MAXW];  // direct tiles: plain 3-D map of the staged payload
@@ -235,16 +275,17 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
 };
 
-__global__ void __launch_bounds__(32 * V2_CW, 3)
+template <class G, bool FUSED, int MINB>
+__global__ void __launch_bounds__(32 * G::CW, MINB)
 k_accumulate_tma(const __grid_constant__ TmaParams P) {
-    constexpr int PP = V2_PP, DD = V2_DD;
+    constexpr int PP = G::PP, DD = G::DD, NST = G::NST;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)V2_NST * V2_STAGE_BYTES);
-    uint64_t* empty = full + V2_NST;
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NST * G::STAGE_BYTES);
+    uint64_t* empty = full + NST;
 
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t q0 = P.lo + (int64_t)blockIdx.x * (PP * V2_CW);
+    const int64_t q0 = P.lo + (int64_t)blockIdx.x * (PP * G::CW);
     const int j0 = blockIdx.y * 32;
     const int k1_0 = blockIdx.z * DD;
     const bool producer = threadIdx.x == 0;
@@ -253,24 +294,24 @@ k_accumulate_tma(const __grid_constant__ TmaParams P) {
     const int R0 = wrap((int)(q0 - k1_0) - (DD - 1), n);
     const int C0 = wrap((int)(q0 - j0) - 31 - (DD - 1), n);
     auto issue = [&](int w) {  // producer lane: both tensor boxes of walker w into stage w % NST
-        const int s = w % V2_NST;
-        mbar_arrive_expect_tx(&full[s], V2_DIR_BYTES + V2_SH_BYTES);
-        unsigned char* st = smem_raw + (size_t)s * V2_STAGE_BYTES;
-        tma_load_3d(st + V2_DIR_OFF, &P.dmap[w], 2 * j0, k1_0, 0, &full[s]);
-        tma_load_3d(st + V2_SH_OFF, &P.smap[w], 2 * (C0 - R0 + n), R0, 0, &full[s]);
+        const int s = w % NST;
+        mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
+        unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
+        tma_load_3d(st + G::DIR_OFF, &P.dmap[w], 2 * j0, k1_0, 0, &full[s]);
+        tma_load_3d(st + G::SH_OFF, &P.smap[w], 2 * (C0 - R0 + n), R0, 0, &full[s]);
     };
 
     if (producer) {
-        for (int s = 0; s < V2_NST; ++s) {
+        for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], V2_CW);
+            mbar_init(&empty[s], G::CW);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int w = 0; w < V2_NST && w < P.nbatch; ++w) issue(w);
+        for (int w = 0; w < NST && w < P.nbatch; ++w) issue(w);
     }
     __syncthreads();
 
-    // ------------- warp w owns planes q0 + 4w .. q0 + 4w + 3 -------------
+    // ------------- warp w owns planes q0 + PP*w .. q0 + PP*w + PP-1 -------------
     const int c = j0 + lane;
     const bool col_ok = c < n;
     const int64_t nn = (int64_t)n * n;
@@ -303,41 +344,48 @@ k_accumulate_tma(const __grid_constant__ TmaParams P) {
     const int sh_o = (PP * warp) * 32 + (31 - lane);  // + j * 32
 #pragma unroll 1
     for (int w = 0; w < P.nbatch; ++w) {
-        const int s = w % V2_NST;
-        mbar_wait(&full[s], (w / V2_NST) & 1);
+        const int s = w % NST;
+        mbar_wait(&full[s], (w / NST) & 1);
         const Cx<double>* dir_u =
-            reinterpret_cast<const Cx<double>*>(smem_raw + (size_t)s * V2_STAGE_BYTES + V2_DIR_OFF);
-        const Cx<double>* dir_d = dir_u + V2_DIR_ELEMS;
+            reinterpret_cast<const Cx<double>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
+        const Cx<double>* dir_d = dir_u + G::DIR_ELEMS;
         const Cx<double>* sh_u =
-            reinterpret_cast<const Cx<double>*>(smem_raw + (size_t)s * V2_STAGE_BYTES + V2_SH_OFF);
-        const Cx<double>* sh_d = sh_u + V2_SH_ELEMS;
+            reinterpret_cast<const Cx<double>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
+        const Cx<double>* sh_d = sh_u + G::SH_ELEMS;
+        // Direct elements first; shifted elements stream diagonal by diagonal
+        // (j = p - d + DD-1), one ahead.
         Stg<double> dv[DD];
-        Stg<double> sv[PP + DD - 1];
 #pragma unroll
         for (int d = 0; d < DD; ++d) {
-            const int o = dir_o + d * (V2_DIRLEN + 1);
-            dv[d] = lds_stg(dir_u + o, dir_d + o);
+            const int o = dir_o + d * (G::DIRLEN + 1);
+            dv[d] = lds_plain(dir_u + o, dir_d + o);
         }
-#pragma unroll
-        for (int j = 0; j < PP + DD - 1; ++j) sv[j] = lds_stg(sh_u + sh_o + j * 32, sh_d + sh_o + j * 32);
+        Stg<double> snext = lds_plain(sh_u + sh_o, sh_d + sh_o);
         // Producer duty (lane 0 of warp 0): refill the stage every warp released in
         // the previous iteration with walker w - 1 + NST; its TMA overlaps this math.
-        if (producer && w >= 1 && w - 1 + V2_NST < P.nbatch) {
+        if (producer && w >= 1 && w - 1 + NST < P.nbatch) {
             const int wp = w - 1;
-            mbar_wait(&empty[wp % V2_NST], (wp / V2_NST) & 1);
-            issue(wp + V2_NST);
+            mbar_wait(&empty[wp % NST], (wp / NST) & 1);
+            issue(wp + NST);
         }
 #pragma unroll
-        for (int p = 0; p < PP; ++p) {
+        for (int j = 0; j < PP + DD - 1; ++j) {
+            const Stg<double> S = snext;
+            if (j + 1 < PP + DD - 1) snext = lds_plain(sh_u + sh_o + (j + 1) * 32, sh_d + sh_o + (j + 1) * 32);
 #pragma unroll
             for (int d = 0; d < DD; ++d) {
-                const Stg<double>& S = sv[p - d + DD - 1];
+                const int p = j + d - (DD - 1);
+                if (p < 0 || p >= PP) continue;
                 const Stg<double>& D = dv[d];
-                double p1r, p1i, p2r, p2i;
-                cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);  // u * down[k2][k1]
-                cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);  // d * up[k2][k1]
-                acc[p][d].re = add_rn(acc[p][d].re, add_rn(p1r, p2r));
-                acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
+                if constexpr (FUSED) {
+                    update_fused(acc[p][d], S, D);
+                } else {
+                    double p1r, p1i, p2r, p2i;
+                    cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);  // u * down[k2][k1]
+                    cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);  // d * up[k2][k1]
+                    acc[p][d].re = add_rn(acc[p][d].re, add_rn(p1r, p2r));
+                    acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
+                }
             }
         }
         // Release the stage only once its values have been consumed by the math
@@ -363,7 +411,7 @@ struct MapPair {
     CUtensorMap dmap, smap;
 };
 
-static g4_status make_maps(const void* stg, int n, MapPair* out) {
+static g4_status make_maps(const void* stg, int n, int nsh, MapPair* out) {
     static PFN_encodeTiled encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -382,7 +430,7 @@ static g4_status make_maps(const void* stg, int n, MapPair* out) {
     {
         const cuuint64_t dims[3] = {2 * ld, rows, 2};
         const cuuint64_t strides[2] = {ld * 16, plane_b};
-        const cuuint32_t box[3] = {2 * (cuuint32_t)V2_DIRLEN, (cuuint32_t)V2_DD, 2};
+        const cuuint32_t box[3] = {2 * (cuuint32_t)(32 + 4 - 1), 4u, 2};
         CUresult r = encode(&out->dmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(stg), dims,
                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -396,7 +444,7 @@ static g4_status make_maps(const void* stg, int n, MapPair* out) {
     {
         const cuuint64_t dims[3] = {2 * (2 * (cuuint64_t)n + ld), rows, 2};
         const cuuint64_t strides[2] = {(ld + 1) * 16, plane_b};
-        const cuuint32_t box[3] = {64, (cuuint32_t)V2_NSH, 2};
+        const cuuint32_t box[3] = {64, (cuuint32_t)nsh, 2};
         void* base = static_cast<char*>(const_cast<void*>(stg)) - (size_t)n * 16;
         CUresult r = encode(&out->smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
                             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -409,27 +457,28 @@ static g4_status make_maps(const void* stg, int n, MapPair* out) {
     return G4_OK;
 }
 
-static g4_status get_maps(const void* stg, int n, MapPair* out) {
+static g4_status get_maps(const void* stg, int n, int nsh, MapPair* out) {
     static std::mutex mu;
     static std::unordered_map<uint64_t, MapPair> cache;
-    const uint64_t key = reinterpret_cast<uint64_t>(stg) ^ ((uint64_t)n << 48);
+    const uint64_t key = reinterpret_cast<uint64_t>(stg) ^ ((uint64_t)n << 40) ^ ((uint64_t)nsh << 58);
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it != cache.end()) {
         *out = it->second;
         return G4_OK;
     }
-    G4_TRY(make_maps(stg, n, out));
+    G4_TRY(make_maps(stg, n, nsh, out));
     if (cache.size() > 4096) cache.clear();
     cache.emplace(key, *out);
     return G4_OK;
 }
 
+template <class G, bool FUSED, int MINB>
 static g4_status launch_v2(const AccParams<double>& prm, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)V2_SMEM));
+        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<G, FUSED, MINB>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
         attr_set = true;
     }
     const int n = prm.n;
@@ -443,33 +492,62 @@ static g4_status launch_v2(const AccParams<double>& prm, cudaStream_t st) {
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
-            G4_TRY(get_maps(prm.stg[b0 + i], n, &mp));
+            G4_TRY(get_maps(prm.stg[b0 + i], n, G::NSH, &mp));
             tp.dmap[i] = mp.dmap;
             tp.smap[i] = mp.smap;
         }
         const int64_t planes = prm.hi - prm.lo;
-        dim3 grid((unsigned)((planes + V2_PP * V2_CW - 1) / (V2_PP * V2_CW)), (unsigned)((n + 31) / 32),
-                  (unsigned)((n + V2_DD - 1) / V2_DD));
+        dim3 grid((unsigned)((planes + G::PP * G::CW - 1) / (G::PP * G::CW)), (unsigned)((n + 31) / 32),
+                  (unsigned)((n + G::DD - 1) / G::DD));
         if (grid.y > 65535u || grid.z > 65535u)
             return fail(G4_ERR_CONTRACT, "accumulate: N too large for the launch grid");
-        k_accumulate_tma<<<grid, 32 * V2_CW, V2_SMEM, st>>>(tp);
+        k_accumulate_tma<G, FUSED, MINB><<<grid, 32 * G::CW, G::SMEM, st>>>(tp);
         G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
     }
     return G4_OK;
 }
 
+// v2 geometry selection (G4RING_V2GEOM overrides for measurements):
+//   0: PP=4, CW=4, 3 stages, 3 CTAs/SM   1: PP=8, CW=2, 3 stages   2: PP=8, CW=4, 2 stages
+//   3: PP=4, CW=4, 2 stages, 4 CTAs/SM (128 registers) -- the default (fastest measured)
+static int v2_geom() {
+    static int g = -1;
+    if (g < 0) {
+        const char* e = getenv("G4RING_V2GEOM");
+        g = e ? atoi(e) : 3;
+    }
+    return g;
+}
+
+template <bool FUSED>
+static g4_status launch_v2_auto(const AccParams<double>& prm, cudaStream_t st) {
+    switch (v2_geom()) {
+        case 1: return launch_v2<V2Geom<8, 2, 3>, FUSED, 3>(prm, st);
+        case 2: return launch_v2<V2Geom<8, 4, 2>, FUSED, 2>(prm, st);
+        case 0: return launch_v2<V2Geom<4, 4, 3>, FUSED, 3>(prm, st);
+        default: return launch_v2<V2Geom<4, 4, 2>, FUSED, 4>(prm, st);
+    }
+}
+
 // ---------------------------------------------------------------------------
-template <typename R>
-static g4_status dispatch(const AccParams<R>& prm, cudaStream_t st) {
+template <typename R, bool FUSED>
+static g4_status dispatch_t(const AccParams<R>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     const int variant = kernel_variant();
     if constexpr (sizeof(R) == 8) {
-        if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2(prm, st);
-        if (variant == 2 && prm.n >= 64) return launch_v2(prm, st);
+        if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2_auto<FUSED>(prm, st);
+        if (variant == 2 && prm.n >= 64) return launch_v2_auto<FUSED>(prm, st);
     }
-    if (planes <= 4) return launch_v1<R, 4, 4, 1, 12>(prm, st);
-    if (planes <= 8) return launch_v1<R, 4, 4, 2, 6>(prm, st);
-    return launch_v1<R, 4, 4, 4, 3>(prm, st);
+    if (planes <= 4) return launch_v1<R, 4, 4, 1, 12, FUSED>(prm, st);
+    if (planes <= 8) return launch_v1<R, 4, 4, 2, 6, FUSED>(prm, st);
+    return launch_v1<R, 4, 4, 4, 3, FUSED>(prm, st);
+}
+
+static int g_arith = G4_ARITH_EXACT;
+
+template <typename R>
+static g4_status dispatch(const AccParams<R>& prm, cudaStream_t st) {
+    return g_arith == G4_ARITH_FUSED ? dispatch_t<R, true>(prm, st) : dispatch_t<R, false>(prm, st);
 }
 
 template <typename R>
@@ -522,6 +600,13 @@ g4_status g4_set_kernel_variant(int32_t variant) {
     if (variant < 0 || variant > 2)
         return g4::fail(G4_ERR_CONTRACT, "kernel variant must be 0 (auto), 1 (v1) or 2 (v2)");
     g4::g_variant = variant;
+    return G4_OK;
+}
+
+g4_status g4_set_arith_mode(int32_t mode) {
+    if (mode != G4_ARITH_EXACT && mode != G4_ARITH_FUSED)
+        return g4::fail(G4_ERR_CONTRACT, "arith mode must be G4_ARITH_EXACT or G4_ARITH_FUSED");
+    g4::g_arith = mode;
     return G4_OK;
 }
 

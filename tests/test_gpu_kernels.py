@@ -288,3 +288,30 @@ def test_full_size_sampled_planes(oracle, cuda_dev, n, planes):
         for up, down in host:
             oracle.accumulate(ref, q, q + 1, up, down)
         assert np.array_equal(to_np(sl.data), ref), f"plane {q}"
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_fused_arith_within_tolerance(oracle, cuda_dev, variant):
+    """G4_ARITH_FUSED: integer-valued payloads stay bitwise; float within 1e-12 relative."""
+    lib = _lib.load()
+    _lib.check(lib.g4_set_kernel_variant(variant))
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED))
+    try:
+        sp = T.CombinedIndexSpace(8, 16)
+        n, lo, hi = sp.size, 30, 70
+        for mode in ("integer", "float"):
+            sl = T.GtSlice.zeros(sp, lo, hi, device=cuda_dev)
+            gs = [T.generate_gsigma(5, T.Origin(0, 0, w, 0, 0), sp, mode, device=cuda_dev) for w in range(6)]
+            T.accumulate_g4_batch(sl, gs)
+            ref = np.zeros((hi - lo, n, n), np.complex128)
+            for g in gs:
+                oracle.accumulate(ref, lo, hi, to_np(g.up.contiguous()), to_np(g.down.contiguous()))
+            got = to_np(sl.data)
+            if mode == "integer":
+                assert np.array_equal(got, ref)
+            else:
+                np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+                assert not np.array_equal(got, ref)  # it really is the other evaluation order
+    finally:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
+        _lib.check(lib.g4_set_kernel_variant(0))
