@@ -42,6 +42,9 @@ CONFIGS = {
     "c3": (16, 64, 64, "Nc=16, 64 freqs, 64 exchange planes"),
     "c4": (36, 128, 576, "Nc=36 (6x6), 128 freqs, 36 k x 16 w exchange planes"),
 }
+# a single GPU cannot hold config 4's 196 GB G4: at N=1 it runs the per-GPU share of
+# the 8-GPU ring (576 / 8 = 72 planes, 24.5 GB) -- stated in the JSON config
+SINGLE_GPU_PLANES = {"c4": 72}
 
 
 def measured_peaks():
@@ -230,6 +233,11 @@ def run_gpu(args):
     lib = _lib.load()
     _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if args.arith == "fused" else _lib.G4_ARITH_EXACT))
     n_k, n_w, planes, desc = CONFIGS[args.config]
+    if args.config in SINGLE_GPU_PLANES:
+        planes = SINGLE_GPU_PLANES[args.config]
+        desc += f" -- per-GPU share on one GPU: {planes} planes"
+    if args.planes:
+        planes = args.planes
     sp = T.CombinedIndexSpace(n_k, n_w)
     n = sp.size
     dtype = torch.complex128 if args.dtype == "c128" else torch.complex64
@@ -518,6 +526,7 @@ def main():
     ap.add_argument("--arith", default="exact", choices=["exact", "fused"],
                     help="exact: reference op order (bitwise); fused: FMA-chained (within 1e-10)")
     ap.add_argument("--cpu-steps", type=int, default=3)
+    ap.add_argument("--planes", type=int, default=0, help="override the exchange-plane count (N=1)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":

@@ -63,6 +63,34 @@ struct AccParams {
     const Cx<R>* stg[G4_MAX_BATCH];  // staged payloads (2 x ROWS x LD)
 };
 
+// L2-aware CTA order.  A 1-D grid is walked in blocks of TILE_BY column chunks x
+// TILE_BZ row groups (plane chunks fastest inside a block): every CTA that needs
+// a given payload row segment (direct tile or K3-diagonal band) then runs within
+// a few waves of the others, so the payload rows stay L2-resident even when one
+// staged payload is far larger than L2 (N = 4608: 0.7 GB per walker).
+constexpr int TILE_BY = 16, TILE_BZ = 32;
+
+struct TileCoord {
+    int x, y, z;
+};
+
+__device__ __forceinline__ TileCoord tile_coord(unsigned lin, int nx, int ny, int nz) {
+    const unsigned per_row = (unsigned)nx * ny * TILE_BZ;  // CTAs in a full block row
+    const int br = (int)(lin / per_row);
+    unsigned r = lin - (unsigned)br * per_row;
+    const int bze = min(TILE_BZ, nz - br * TILE_BZ);
+    const unsigned per_blk = (unsigned)nx * TILE_BY * bze;
+    const int by = (int)(r / per_blk);
+    r -= (unsigned)by * per_blk;
+    const int bye = min(TILE_BY, ny - by * TILE_BY);
+    TileCoord t;
+    t.x = (int)(r % nx);
+    r /= nx;
+    t.y = by * TILE_BY + (int)(r % bye);
+    t.z = br * TILE_BZ + (int)(r / bye);
+    return t;
+}
+
 __device__ __forceinline__ int wrap(int x, int n) {
     while (x < 0) x += n;
     while (x >= n) x -= n;
@@ -96,11 +124,13 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
     const int n = P.n;
     const int ld = staged_ld(n);
     const int64_t plane_s = staged_plane(n);
-    const int k1_0 = blockIdx.z * DD;
-    const int c_raw = blockIdx.y * 32 + threadIdx.x;
+    const int nx = (int)((P.hi - P.lo + PP * WARPS - 1) / (PP * WARPS));
+    const TileCoord tc = tile_coord(blockIdx.x, nx, (n + 31) / 32, (n + DD - 1) / DD);
+    const int k1_0 = tc.z * DD;
+    const int c_raw = tc.y * 32 + threadIdx.x;
     const bool col_ok = c_raw < n;
     const int c = col_ok ? c_raw : 0;
-    const int64_t q0 = P.lo + ((int64_t)blockIdx.x * WARPS + threadIdx.y) * PP;
+    const int64_t q0 = P.lo + ((int64_t)tc.x * WARPS + threadIdx.y) * PP;
     if (q0 >= P.hi) return;  // warp-uniform
 
     // Direct elements stg[k1_0 + d][(c + d) % N]; G4 offsets (k1_0 + d) * N + (c + d) % N.
@@ -184,12 +214,10 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
 template <typename R, int PP, int DD, int WARPS, int MINB, bool FUSED>
 static g4_status launch_v1(const AccParams<R>& prm, cudaStream_t st) {
     const int n = prm.n;
-    const int64_t chunks = (prm.hi - prm.lo + PP - 1) / PP;
-    dim3 grid((unsigned)((chunks + WARPS - 1) / WARPS), (unsigned)((n + 31) / 32),
-              (unsigned)((n + DD - 1) / DD));
-    if (grid.y > 65535u || grid.z > 65535u)
-        return fail(G4_ERR_CONTRACT, "accumulate: N too large for the launch grid");
-    k_accumulate<R, PP, DD, WARPS, MINB, FUSED><<<grid, dim3(32, WARPS), 0, st>>>(prm);
+    const int64_t nx = (prm.hi - prm.lo + PP * WARPS - 1) / (PP * WARPS);
+    const uint64_t ctas = (uint64_t)nx * ((n + 31) / 32) * ((n + DD - 1) / DD);
+    if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
+    k_accumulate<R, PP, DD, WARPS, MINB, FUSED><<<(unsigned)ctas, dim3(32, WARPS), 0, st>>>(prm);
     return check_cuda(cudaGetLastError(), "k_accumulate launch");
 }
 
@@ -273,6 +301,7 @@ struct alignas(64) TmaParams {
     int64_t lo, hi;
     int32_t n;
     int32_t nbatch;
+    int32_t nx;  // plane chunks
 };
 
 template <class G, bool FUSED, int MINB>
@@ -285,9 +314,10 @@ k_accumulate_tma(const __grid_constant__ TmaParams P) {
 
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t q0 = P.lo + (int64_t)blockIdx.x * (PP * G::CW);
-    const int j0 = blockIdx.y * 32;
-    const int k1_0 = blockIdx.z * DD;
+    const TileCoord tc = tile_coord(blockIdx.x, P.nx, (n + 31) / 32, (n + DD - 1) / DD);
+    const int64_t q0 = P.lo + (int64_t)tc.x * (PP * G::CW);
+    const int j0 = tc.y * 32;
+    const int k1_0 = tc.z * DD;
     const bool producer = threadIdx.x == 0;
     // band origin: row R0 = (q0 - k1_0 - (DD-1)) mod N, column C0 = (q0 - j0 - 31 - (DD-1)) mod N;
     // sheared coordinates (c1, c2) = (C0 - R0 + N, R0) (see make_maps).
@@ -497,11 +527,10 @@ static g4_status launch_v2(const AccParams<double>& prm, cudaStream_t st) {
             tp.smap[i] = mp.smap;
         }
         const int64_t planes = prm.hi - prm.lo;
-        dim3 grid((unsigned)((planes + G::PP * G::CW - 1) / (G::PP * G::CW)), (unsigned)((n + 31) / 32),
-                  (unsigned)((n + G::DD - 1) / G::DD));
-        if (grid.y > 65535u || grid.z > 65535u)
-            return fail(G4_ERR_CONTRACT, "accumulate: N too large for the launch grid");
-        k_accumulate_tma<G, FUSED, MINB><<<grid, 32 * G::CW, G::SMEM, st>>>(tp);
+        tp.nx = (int32_t)((planes + G::PP * G::CW - 1) / (G::PP * G::CW));
+        const uint64_t ctas = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DD - 1) / G::DD);
+        if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
+        k_accumulate_tma<G, FUSED, MINB><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
         G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
     }
     return G4_OK;
