@@ -21,7 +21,9 @@
  *     g4_prepare_g / g4_generate, consumed by g4_accumulate_staged, and the form
  *     that travels around the ring): spin-planar transposes with a cyclic halo,
  *       stg[s][r][c] = M_s[c mod N][r mod N],   s = 0 (up), 1 (down),
- *       0 <= r < N + G4_HALO_ROWS,  0 <= c < LD = N + G4_HALO_COLS  (row pitch LD).
+ *       0 <= r < N + G4_HALO_ROWS,  0 <= c < LD  (row pitch LD),
+ *       LD = N + G4_HALO_COLS, plus 1 for complex64 when that is even (the
+ *       diagonal TMA stride (LD + 1) * 8 B must be a multiple of 16 B).
  *     The core stg[s][0:N][0:N] is the transpose of the reference matrix; the
  *     halo replicates it cyclically so that every window the update kernel
  *     fetches (TMA boxes along rows and along the K3-diagonal) is contiguous.
@@ -71,11 +73,11 @@ const char* g4_last_error(void);
 /* G4RING_ABI_VERSION of the loaded library. */
 int32_t g4_abi_version(void);
 /* Bytes of one walker payload in the staged device layout:
- * 2 * (n + G4_HALO_ROWS) * (n + G4_HALO_COLS) * entry bytes (the reference's
- * GSigma.nbytes, tensor.py:86-89, is the 2 * n * n core of it). */
+ * 2 * ROWS * LD * entry bytes (the reference's GSigma.nbytes, tensor.py:86-89,
+ * is the 2 * n * n core of it). */
 int64_t g4_payload_bytes(int32_t n, int32_t dtype);
-/* Staged-layout geometry: rows per spin plane and row pitch (elements). */
-g4_status g4_staged_dims(int32_t n, int32_t* rows, int32_t* ld);
+/* Staged-layout geometry for a dtype: rows per spin plane and row pitch (elements). */
+g4_status g4_staged_dims(int32_t n, int32_t dtype, int32_t* rows, int32_t* ld);
 
 /* Cyclic K difference (a - b) mod n; replaces index_diff (tensor.py:50-55).
  * Out-of-range a or b -> G4_ERR_CONTRACT. */

@@ -33,7 +33,7 @@ SIGNATURES = {
     "g4_last_error": (ctypes.c_char_p, []),
     "g4_abi_version": (_i32, []),
     "g4_payload_bytes": (_i64, [_i32, _i32]),
-    "g4_staged_dims": (_i32, [_i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
+    "g4_staged_dims": (_i32, [_i32, _i32, ctypes.POINTER(_i32), ctypes.POINTER(_i32)]),
     "g4_index_diff": (_i32, [_i64, _i64, _i64, _i64p]),
     "g4_make_partition": (_i32, [_i64, _i64, _i64p]),
     "g4_prepare_g": (_i32, [_vpp, _vpp, _vpp, _i32, _i32, _i32, _i32, _vp]),

@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include "../../include/g4ring.h"
+#include "g4_layout.h"
 
 namespace g4 {
 
@@ -32,19 +33,6 @@ template <typename R>
 struct alignas(2 * sizeof(R)) Cx {
     R re, im;
 };
-
-// Staged layout of one walker payload in memory (include/g4ring.h): spin-planar
-// transposes with a cyclic halo,
-//   stg[s][r][c] = M_s[c mod N][r mod N],  s = 0 (up), 1 (down),
-//   r < ROWS = N + G4_HALO_ROWS,  c < LD = N + G4_HALO_COLS,
-// so every operand row of the update is contiguous, every 16-B (c128) half is
-// a contiguous stream in global and shared memory, and any window of up to
-// HALO rows / cols starting inside the core never wraps (TMA boxes).
-__host__ __device__ __forceinline__ int staged_ld(int n) { return n + G4_HALO_COLS; }
-__host__ __device__ __forceinline__ int staged_rows(int n) { return n + G4_HALO_ROWS; }
-__host__ __device__ __forceinline__ int64_t staged_plane(int n) {
-    return (int64_t)staged_rows(n) * staged_ld(n);
-}
 
 // One staged walker element in registers: (u, d) = (up^T, down^T) at one (row, col).
 template <typename R>

@@ -3,6 +3,7 @@
 #include <string>
 
 #include "g4_internal.h"
+#include "g4_layout.h"
 
 namespace g4 {
 
@@ -27,13 +28,14 @@ int32_t g4_abi_version(void) { return G4RING_ABI_VERSION; }
 
 int64_t g4_payload_bytes(int32_t n, int32_t dtype) {
     if (n < 1 || (dtype != G4_C128 && dtype != G4_C64)) return -1;
-    return 2 * (int64_t)(n + G4_HALO_ROWS) * (n + G4_HALO_COLS) * g4::entry_bytes(dtype);
+    return 2 * g4::staged_plane(n, (int)g4::entry_bytes(dtype)) * g4::entry_bytes(dtype);
 }
 
-g4_status g4_staged_dims(int32_t n, int32_t* rows, int32_t* ld) {
-    if (n < 1 || !rows || !ld) return g4::fail(G4_ERR_CONTRACT, "staged_dims: bad arguments");
-    *rows = n + G4_HALO_ROWS;
-    *ld = n + G4_HALO_COLS;
+g4_status g4_staged_dims(int32_t n, int32_t dtype, int32_t* rows, int32_t* ld) {
+    if (n < 1 || !rows || !ld || (dtype != G4_C128 && dtype != G4_C64))
+        return g4::fail(G4_ERR_CONTRACT, "staged_dims: bad arguments");
+    *rows = g4::staged_rows(n);
+    *ld = g4::staged_ld(n, (int)g4::entry_bytes(dtype));
     return G4_OK;
 }
 

@@ -256,9 +256,9 @@ class RingEngine:
         self.channels = S.make_channels(self.topo, self.pos)
         self.lib = _lib.load()
         # per channel: 3 buffers (GEN, R0, R1) x batch x lanes staged payloads
-        self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n), dtype=self.dtype,
+        self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n, self.dtype), dtype=self.dtype,
                                  device=device) for c in self.channels]
-        self.payload_bytes = int(np.prod(staged_shape(n))) * self.bufs[0].element_size()
+        self.payload_bytes = int(np.prod(staged_shape(n, self.dtype))) * self.bufs[0].element_size()
         self.flags = torch.zeros(len(self.channels) * S.FLAGS_PER_CHANNEL, dtype=torch.int64, device=device)
         self.compute = torch.cuda.Stream(device)
         self.comm = [torch.cuda.Stream(device) for _ in self.channels]

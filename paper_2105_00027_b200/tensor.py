@@ -23,7 +23,8 @@ oracle_accumulate      oracle_accumulate         (276-283)   K3 + K1 in canonica
 Differences, all deliberate:
 * ``GtSlice.data`` is a CUDA ``torch.Tensor`` (complex128, or complex64) with the
   reference's exact layout ``data[k3 - lo, k1, k2]``.
-* ``GSigma`` stores one device tensor ``staged`` of shape (2, N + 32, N + 64):
+* ``GSigma`` stores one device tensor ``staged`` of shape (2, N + 40, LD), LD = N + 72
+  (odd for complex64):
   spin-planar transposes with a cyclic halo, ``staged[s, r, c] = M_s[c % N, r % N]``
   (``M_0 = up``, ``M_1 = down``) -- the layout the update kernel reads
   row-contiguously (and with TMA boxes) and the form that travels around the ring.  ``g.up`` and
@@ -48,9 +49,12 @@ _MODE_CODE = {"float": _lib.G4_MODE_FLOAT, "integer": _lib.G4_MODE_INTEGER}
 _DTYPE_CODE = {torch.complex128: _lib.G4_C128, torch.complex64: _lib.G4_C64}
 
 
-def staged_shape(n: int) -> tuple[int, int, int]:
-    """Shape of one staged payload (include/g4ring.h): (2, N + HALO_ROWS, N + HALO_COLS)."""
-    return (2, n + _lib.G4_HALO_ROWS, n + _lib.G4_HALO_COLS)
+def staged_shape(n: int, dtype: torch.dtype = torch.complex128) -> tuple[int, int, int]:
+    """Shape of one staged payload (include/g4ring.h): (2, ROWS, LD) from g4_staged_dims."""
+    lib = _lib.load()
+    rows, ld = ctypes.c_int32(), ctypes.c_int32()
+    _lib.check(lib.g4_staged_dims(n, _dtype_code(dtype), ctypes.byref(rows), ctypes.byref(ld)), "staged_dims")
+    return (2, rows.value, ld.value)
 
 
 def _stream_ptr(device: torch.device) -> int:
@@ -130,13 +134,13 @@ class GSigma:
         n = space.size
         if staged is not None:
             _require_cuda(staged, "GSigma.staged")
-            if tuple(staged.shape) != staged_shape(n) or not staged.is_contiguous():
-                raise ContractViolation(f"staged payload must be contiguous {staged_shape(n)}")
+            if tuple(staged.shape) != staged_shape(n, staged.dtype) or not staged.is_contiguous():
+                raise ContractViolation(f"staged payload must be contiguous {staged_shape(n, staged.dtype)}")
             _dtype_code(staged.dtype)
             self.staged = staged
             return
         dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.staged = torch.empty(staged_shape(n), dtype=dtype, device=dev)
+        self.staged = torch.empty(staged_shape(n, dtype), dtype=dtype, device=dev)
         if up is None and down is None:
             self.staged.zero_()
             return

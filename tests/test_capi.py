@@ -33,7 +33,7 @@ def test_library_exports_every_header_symbol():
 def test_payload_bytes():
     lib = _lib.load()
     assert lib.g4_payload_bytes(512, _lib.G4_C128) == 2 * 552 * 584 * 16
-    assert lib.g4_payload_bytes(4608, _lib.G4_C64) == 2 * 4648 * 4680 * 8
+    assert lib.g4_payload_bytes(4608, _lib.G4_C64) == 2 * 4648 * 4681 * 8  # odd pitch for complex64
     assert lib.g4_payload_bytes(0, _lib.G4_C128) == -1
 
 

@@ -119,7 +119,7 @@ def test_prepare_is_exact_transpose(cuda_dev):
         down = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
         g = payload(up, down, cuda_dev)
         st = to_np(g.staged)
-        assert st.shape == T.staged_shape(n)
+        assert st.shape == T.staged_shape(n, torch.complex128)
         assert np.array_equal(st[0, :n, :n], up.T) and np.array_equal(st[1, :n, :n], down.T)
         rr, cc = np.meshgrid(np.arange(st.shape[1]) % n, np.arange(st.shape[2]) % n, indexing="ij")
         assert np.array_equal(st[0], up.T[rr, cc]) and np.array_equal(st[1], down.T[rr, cc])  # halo
@@ -217,9 +217,19 @@ def test_contract_violations(cuda_dev):
         _lib.check(st)
 
 
-def test_complex64(oracle, cuda_dev):
+@pytest.mark.parametrize("n,lo,hi,variant", [(48, 10, 18, 0), (160, 5, 40, 0), (160, 5, 40, 1),
+                                             (257, 240, 257, 2), (96, 0, 96, 2)])
+def test_complex64(oracle, cuda_dev, n, lo, hi, variant):
+    lib = _lib.load()
+    _lib.check(lib.g4_set_kernel_variant(variant))
+    try:
+        _complex64_case(oracle, cuda_dev, n, lo, hi)
+    finally:
+        _lib.check(lib.g4_set_kernel_variant(0))
+
+
+def _complex64_case(oracle, cuda_dev, n, lo, hi):
     rng = np.random.default_rng(8)
-    n, lo, hi = 48, 10, 18
     sp = T.CombinedIndexSpace(1, n)
     ref128 = np.zeros((hi - lo, n, n), np.complex128)
     ref64 = np.zeros((hi - lo, n, n), np.complex64)
