@@ -265,15 +265,20 @@ struct V2Geom {
     static constexpr int PP = PP_, DD = 4, CW = CW_, NST = NST_;
     static constexpr int ES = sizeof(Cx<R>);                      // bytes per complex entry
     static constexpr int NSH = PP * CW + DD - 1;                  // shifted row segments (band height)
-    static constexpr int DIR_ELEMS = DD * 32;                     // per spin (sheared direct box)
-    static constexpr int SH_ELEMS = NSH * 32;                     // per spin
+    // Box row width in entries.  A TMA box must start on a 16-B boundary along
+    // its innermost dimension (tools/tma_probe.cu: odd 8-B starts fault), so for
+    // complex64 boxes start at the even entry below and carry 2 extra entries;
+    // consumers add the start's parity (0 or 1).
+    static constexpr int W = ES == 8 ? 34 : 32;
+    static constexpr int DIR_ELEMS = DD * W;                      // per spin (sheared direct box)
+    static constexpr int SH_ELEMS = NSH * W;                      // per spin
     static constexpr uint32_t DIR_BYTES = 2 * DIR_ELEMS * ES;     // both spins
     static constexpr uint32_t SH_BYTES = 2 * SH_ELEMS * ES;
     static constexpr uint32_t DIR_OFF = 0;
     static constexpr uint32_t SH_OFF = (DIR_BYTES + 127) / 128 * 128;
     static constexpr uint32_t STAGE_BYTES = (SH_OFF + SH_BYTES + 127) / 128 * 128;
     static constexpr size_t SMEM = (size_t)NST * STAGE_BYTES + 2 * NST * sizeof(uint64_t);
-    static_assert(NSH <= G4_HALO_ROWS && NSH + 31 < G4_HALO_COLS, "halo too small for the v2 band");
+    static_assert(NSH <= G4_HALO_ROWS && NSH + W + 1 < G4_HALO_COLS, "halo too small for the v2 band");
 };
 
 template <typename R>
@@ -333,12 +338,14 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     //    R0 = (q0 - k1_0 - (DD-1)) mod N, C0 = (q0 - j0 - 31 - (DD-1)) mod N  -> (C0 - R0 + off, R0)
     const int R0 = wrap((int)(q0 - k1_0) - (DD - 1), n);
     const int C0 = wrap((int)(q0 - j0) - 31 - (DD - 1), n);
+    const int xd = j0 - k1_0 + P.off, xs = C0 - R0 + P.off;  // box starts (entries, >= 0)
+    const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;  // 16-B alignment shift
     auto issue = [&](int w) {  // producer lane: both tensor boxes of walker w into stage w % NST
         const int s = w % NST;
         mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
         unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
-        tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (j0 - k1_0 + P.off), k1_0, 0, &full[s]);
-        tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (C0 - R0 + P.off), R0, 0, &full[s]);
+        tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), k1_0, 0, &full[s]);
+        tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
     };
 
     if (producer) {
@@ -380,7 +387,8 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         }
 
     // shared-memory element offsets (complex units) inside a stage
-    const int sh_o = (PP * warp) * 32 + (31 - lane);  // + j * 32
+    const int sh_o = (PP * warp) * G::W + (31 - lane) + ps;  // + j * W
+    const int dr_o = lane + pd;                               // + d * W
 #pragma unroll 1
     for (int w = 0; w < P.nbatch; ++w) {
         const int s = w % NST;
@@ -393,7 +401,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         // stream diagonal by diagonal (j = p - d + DD-1), one ahead.
         Stg<R> dv[DD];
 #pragma unroll
-        for (int d = 0; d < DD; ++d) dv[d] = lds_plain(dir_u + d * 32 + lane, dir_d + d * 32 + lane);
+        for (int d = 0; d < DD; ++d) dv[d] = lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o);
         Stg<R> snext = lds_plain(sh_u + sh_o, sh_d + sh_o);
         // Producer duty (lane 0 of warp 0): refill the stage every warp released in
         // the previous iteration with walker w - 1 + NST; its TMA overlaps this math.
@@ -405,7 +413,8 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
 #pragma unroll
         for (int j = 0; j < PP + DD - 1; ++j) {
             const Stg<R> S = snext;
-            if (j + 1 < PP + DD - 1) snext = lds_plain(sh_u + sh_o + (j + 1) * 32, sh_d + sh_o + (j + 1) * 32);
+            if (j + 1 < PP + DD - 1)
+                snext = lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W);
 #pragma unroll
             for (int d = 0; d < DD; ++d) {
                 const int p = j + d - (DD - 1);
@@ -449,7 +458,7 @@ struct MapPair {
 // is non-negative, and the map's base (stg - off * es) stays 16-B aligned.
 static int sheared_offset(int n, int es) { return (es == 8 && (n & 1)) ? n + 1 : n; }
 
-static g4_status make_maps(const void* stg, int n, int es, int nsh, MapPair* out) {
+static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, MapPair* out) {
     static PFN_encodeTiled encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -459,7 +468,7 @@ static g4_status make_maps(const void* stg, int n, int es, int nsh, MapPair* out
             return fail(G4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
         encode = reinterpret_cast<PFN_encodeTiled>(fn);
     }
-    const cuuint64_t ld = (cuuint64_t)staged_ld(n, es), rows = (cuuint64_t)staged_rows(n);
+    const cuuint64_t ld = (cuuint64_t)staged_ld(n, es), rows = (cuuint64_t)staged_rows(n, es);
     const cuuint64_t plane_b = (cuuint64_t)staged_plane(n, es) * es;
     const cuuint32_t ew = es / 8;  // 64-bit elements per complex entry
     const int off = sheared_offset(n, es);
@@ -473,7 +482,7 @@ static g4_status make_maps(const void* stg, int n, int es, int nsh, MapPair* out
     const cuuint32_t estr[3] = {1, 1, 1};
     void* base = static_cast<char*>(const_cast<void*>(stg)) - (size_t)off * es;
     for (int which = 0; which < 2; ++which) {
-        const cuuint32_t box[3] = {32 * ew, which == 0 ? 4u : (cuuint32_t)nsh, 2};
+        const cuuint32_t box[3] = {(cuuint32_t)width * ew, which == 0 ? 4u : (cuuint32_t)nsh, 2};
         CUresult r = encode(which == 0 ? &out->dmap : &out->smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base,
                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -486,7 +495,7 @@ static g4_status make_maps(const void* stg, int n, int es, int nsh, MapPair* out
     return G4_OK;
 }
 
-static g4_status get_maps(const void* stg, int n, int es, int nsh, MapPair* out) {
+static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, MapPair* out) {
     static std::mutex mu;
     static std::map<std::tuple<uintptr_t, int, int, int>, MapPair> cache;
     const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(stg), n, nsh, es);
@@ -496,7 +505,7 @@ static g4_status get_maps(const void* stg, int n, int es, int nsh, MapPair* out)
         *out = it->second;
         return G4_OK;
     }
-    G4_TRY(make_maps(stg, n, es, nsh, out));
+    G4_TRY(make_maps(stg, n, es, nsh, width, out));
     if (cache.size() > 4096) cache.clear();
     cache.emplace(key, *out);
     return G4_OK;
@@ -522,7 +531,7 @@ static g4_status launch_v2(const AccParams<R>& prm, cudaStream_t st) {
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
-            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, &mp));
+            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, &mp));
             tp.dmap[i] = mp.dmap;
             tp.smap[i] = mp.smap;
         }
@@ -563,12 +572,8 @@ template <typename R, bool FUSED>
 static g4_status dispatch_t(const AccParams<R>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     const int variant = kernel_variant();
-    // complex64 stays on v1 for now: its TMA variant faults (under investigation,
-    // tools/tma_probe.cu); complex128 uses v2.
-    if constexpr (sizeof(R) == 8) {
-        if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2_auto<R, FUSED>(prm, st);
-        if (variant == 2 && prm.n >= 64) return launch_v2_auto<R, FUSED>(prm, st);
-    }
+    if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2_auto<R, FUSED>(prm, st);
+    if (variant == 2 && prm.n >= 64) return launch_v2_auto<R, FUSED>(prm, st);
     if (planes <= 4) return launch_v1<R, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, 4, 4, 4, 3, FUSED>(prm, st);

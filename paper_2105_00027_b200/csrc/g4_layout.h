@@ -21,7 +21,11 @@ G4_HD int staged_ld(int n, int eb) {
     const int ld = n + G4_HALO_COLS;
     return (eb == 8 && (ld % 2) == 0) ? ld + 1 : ld;
 }
-G4_HD int staged_rows(int n) { return n + G4_HALO_ROWS; }
-G4_HD int64_t staged_plane(int n, int eb) { return (int64_t)staged_rows(n) * staged_ld(n, eb); }
+// For complex64 the row count is even so the spin-plane stride is a 16-B multiple.
+G4_HD int staged_rows(int n, int eb) {
+    const int rows = n + G4_HALO_ROWS;
+    return (eb == 8 && (rows % 2) != 0) ? rows + 1 : rows;
+}
+G4_HD int64_t staged_plane(int n, int eb) { return (int64_t)staged_rows(n, eb) * staged_ld(n, eb); }
 
 }  // namespace g4

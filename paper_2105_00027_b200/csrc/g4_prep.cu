@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) k_prepare(const __grid_constant__ PrepPar
     __shared__ Cx<Rin> su[32][33];
     __shared__ Cx<Rin> sd[32][33];
     const int n = P.n;
-    const int ld = staged_ld(n, sizeof(Cx<Rout>)), rows = staged_rows(n);
+    const int ld = staged_ld(n, sizeof(Cx<Rout>)), rows = staged_rows(n, sizeof(Cx<Rout>));
     const int w = blockIdx.z;
     const int r0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
     const Cx<Rin>* up = P.up[w];
@@ -79,7 +79,7 @@ static g4_status prepare_t(void* const* staged, const void* const* up, const voi
             prm.stg[i] = static_cast<Cx<Rout>*>(staged[b0 + i]);
         }
         prm.n = n;
-        const unsigned tr = (unsigned)((staged_rows(n) + 31) / 32),
+        const unsigned tr = (unsigned)((staged_rows(n, sizeof(Cx<Rout>)) + 31) / 32),
                        tc = (unsigned)((staged_ld(n, sizeof(Cx<Rout>)) + 31) / 32);
         if (tr > 65535u || tc > 65535u) return fail(G4_ERR_CONTRACT, "prepare_g: N too large");
         k_prepare<Rin, Rout><<<dim3(tr, tc, nb), dim3(32, 8), 0, st>>>(prm);
@@ -129,7 +129,7 @@ __device__ __forceinline__ void gen_entry(uint64_t key, uint64_t idx, int mode, 
 template <typename R>
 __global__ void __launch_bounds__(256) k_generate_staged(const __grid_constant__ GenParams<R> P) {
     const int n = P.n, w = blockIdx.z;
-    const int ld = staged_ld(n, sizeof(Cx<R>)), rows = staged_rows(n);
+    const int ld = staged_ld(n, sizeof(Cx<R>)), rows = staged_rows(n, sizeof(Cx<R>));
     const int c = blockIdx.x * 32 + threadIdx.x;
     const int r = blockIdx.y * 8 + threadIdx.y;
     if (c >= ld || r >= rows) return;
@@ -200,7 +200,7 @@ static g4_status generate_t(void* const* staged, void* const* up, void* const* d
         if (any_stg) {
             for (int i = 0; i < nb; ++i)
                 if (!prm.stg[i]) return fail(G4_ERR_CONTRACT, "generate: staged list has a null entry");
-            dim3 grid((unsigned)((staged_ld(n, sizeof(Cx<R>)) + 31) / 32), (unsigned)((staged_rows(n) + 7) / 8),
+            dim3 grid((unsigned)((staged_ld(n, sizeof(Cx<R>)) + 31) / 32), (unsigned)((staged_rows(n, sizeof(Cx<R>)) + 7) / 8),
                       nb);
             if (grid.y > 65535u) return fail(G4_ERR_CONTRACT, "generate: N too large");
             k_generate_staged<R><<<grid, dim3(32, 8), 0, st>>>(prm);

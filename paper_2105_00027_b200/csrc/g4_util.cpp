@@ -34,7 +34,7 @@ int64_t g4_payload_bytes(int32_t n, int32_t dtype) {
 g4_status g4_staged_dims(int32_t n, int32_t dtype, int32_t* rows, int32_t* ld) {
     if (n < 1 || !rows || !ld || (dtype != G4_C128 && dtype != G4_C64))
         return g4::fail(G4_ERR_CONTRACT, "staged_dims: bad arguments");
-    *rows = g4::staged_rows(n);
+    *rows = g4::staged_rows(n, (int)g4::entry_bytes(dtype));
     *ld = g4::staged_ld(n, (int)g4::entry_bytes(dtype));
     return G4_OK;
 }
