@@ -240,11 +240,13 @@ def run_gpu(args):
         planes = args.planes
     sp = T.CombinedIndexSpace(n_k, n_w)
     n = sp.size
-    dtype = torch.complex128 if args.dtype == "c128" else torch.complex64
-    eb = 16 if args.dtype == "c128" else 8
+    dtype = torch.complex64 if args.dtype == "c64" else torch.complex128    # G4 slice
+    pdtype = torch.complex128 if args.dtype == "c128" else torch.complex64  # payloads
+    eb = 16 if dtype == torch.complex128 else 8
+    peb = 16 if pdtype == torch.complex128 else 8
     B = args.batch
     sl = T.GtSlice.zeros(sp, 0, planes, device=dev, dtype=dtype)
-    pools = [[T.GSigma.empty(sp, device=dev, dtype=dtype) for _ in range(B)] for _ in range(2)]
+    pools = [[T.GSigma.empty(sp, device=dev, dtype=pdtype) for _ in range(B)] for _ in range(2)]
     for i, pool in enumerate(pools):
         T.fill_gsigmas(pool, 0, [T.Origin(0, 0, w, i, 0) for w in range(B)], "float")
     stream = torch.cuda.current_stream(dev)
@@ -273,7 +275,7 @@ def run_gpu(args):
     upd_step = B * planes * n * n
     value = upd_step * args.steps / (total_ms * 1e-3)
     peak, peak_kind = measured_peaks()
-    alg_bytes = 2 * planes * n * n * eb + B * 2 * n * n * eb
+    alg_bytes = 2 * planes * n * n * eb + B * 2 * n * n * peb
     achieved = alg_bytes / (statistics.mean(k_ms) * 1e-3) / 1e9
 
     # -- e2e: reference-layout payloads in pinned host memory through g4_accumulate --
@@ -314,7 +316,7 @@ def run_e2e(args, lib, T, sp, planes, dtype, eb, dev):
     import torch
     n = sp.size
     B = args.batch
-    code = _dtype_code(dtype)
+    code = 2 if args.dtype == "mixed" else _dtype_code(dtype)  # G4_C128_G64 for mixed
     sl = T.GtSlice.zeros(sp, 0, planes, device=dev, dtype=dtype)
     host = []
     for i in range(2):
@@ -522,7 +524,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--batch", type=int, default=8, help="walkers per K1 pass (per rank)")
-    ap.add_argument("--dtype", default="c128", choices=["c128", "c64"])
+    ap.add_argument("--dtype", default="c128", choices=["c128", "c64", "mixed"],
+                    help="mixed: complex128 G4 slice with complex64 payloads")
     ap.add_argument("--arith", default="exact", choices=["exact", "fused"],
                     help="exact: reference op order (bitwise); fused: FMA-chained (within 1e-10)")
     ap.add_argument("--cpu-steps", type=int, default=3)

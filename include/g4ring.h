@@ -53,8 +53,11 @@ typedef enum {
 } g4_status;
 
 typedef enum {
-    G4_C128 = 0, /* complex128: ENTRY_BYTES = 16 (tensor.py:23) -- the reference dtype */
-    G4_C64 = 1   /* complex64: the paper's production G_sigma precision; 1e-5 tolerance */
+    G4_C128 = 0,     /* complex128: ENTRY_BYTES = 16 (tensor.py:23) -- the reference dtype */
+    G4_C64 = 1,      /* complex64: the paper's production G_sigma precision; 1e-5 tolerance */
+    G4_C128_G64 = 2  /* mixed: complex128 G4 slice, complex64 payloads (widened exactly;
+                        g4_accumulate takes complex128 up/down and rounds them to complex64)
+                        -- halves payload bytes on the ring and in shared memory */
 } g4_dtype;
 
 typedef enum {

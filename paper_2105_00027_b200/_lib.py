@@ -16,7 +16,7 @@ from .errors import (ConfigError, ContractViolation, DeadlockError, RingAccError
 LIB_PATH = Path(__file__).resolve().parent / "libg4ring.so"
 
 G4_OK, G4_ERR_CONTRACT, G4_ERR_CONFIG, G4_ERR_TRANSPORT, G4_ERR_DEADLOCK, G4_ERR_CUDA = range(6)
-G4_C128, G4_C64 = 0, 1
+G4_C128, G4_C64, G4_C128_G64 = 0, 1, 2
 G4_MODE_FLOAT, G4_MODE_INTEGER = 0, 1
 G4_CHANNEL_EQ1 = 0
 G4_ARITH_EXACT, G4_ARITH_FUSED = 0, 1

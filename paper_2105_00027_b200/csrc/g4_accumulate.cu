@@ -55,14 +55,26 @@ static int kernel_variant() {
     return g_variant;
 }
 
-template <typename R>
+// RA: G4 entry type, RG: payload entry type (RG = float with RA = double is the
+// mixed-precision mode: complex64 payloads widened exactly into complex128 math).
+template <typename RA, typename RG>
 struct AccParams {
-    Cx<R>* g4;
+    Cx<RA>* g4;
     int64_t lo, hi;
     int32_t n;
     int32_t nbatch;
-    const Cx<R>* stg[G4_MAX_BATCH];  // staged payloads (2 x ROWS x LD)
+    const Cx<RG>* stg[G4_MAX_BATCH];  // staged payloads (2 x ROWS x LD)
 };
+
+template <typename To, typename From>
+__device__ __forceinline__ Stg<To> widen(const Stg<From>& v) {
+    Stg<To> r;
+    r.ur = (To)v.ur;
+    r.ui = (To)v.ui;
+    r.dr = (To)v.dr;
+    r.di = (To)v.di;
+    return r;
+}
 
 // L2-aware CTA order.  A 1-D grid is walked in blocks of TILE_BY column chunks x
 // TILE_BZ row groups (plane chunks fastest inside a block): every CTA that needs
@@ -118,13 +130,13 @@ __device__ __forceinline__ void update_fused(Cx<R>& a, const Stg<R>& S, const St
 
 // ---------------------------------------------------------------------------
 // v1
-template <typename R, int PP, int DD, int WARPS, int MINB, bool FUSED>
+template <typename R, typename RG, int PP, int DD, int WARPS, int MINB, bool FUSED>
 __global__ void __launch_bounds__(32 * WARPS, MINB)
-k_accumulate(const __grid_constant__ AccParams<R> P) {
+k_accumulate(const __grid_constant__ AccParams<R, RG> P) {
     constexpr int NS = PP + DD - 1;  // distinct shifted elements per thread
     const int n = P.n;
-    const int ld = staged_ld(n, sizeof(Cx<R>));
-    const int64_t plane_s = staged_plane(n, sizeof(Cx<R>));
+    const int ld = staged_ld(n, sizeof(Cx<RG>));
+    const int64_t plane_s = staged_plane(n, sizeof(Cx<RG>));
     const int nx = (int)((P.hi - P.lo + PP * WARPS - 1) / (PP * WARPS));
     const TileCoord tc = tile_coord(blockIdx.x, nx, (n + 31) / 32, (n + DD - 1) / DD);
     const int k1_0 = tc.z * DD;
@@ -177,15 +189,15 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
 
 #pragma unroll 1
     for (int w = 0; w < P.nbatch; ++w) {
-        const Cx<R>* su = P.stg[w];
-        const Cx<R>* sd = su + plane_s;
+        const Cx<RG>* su = P.stg[w];
+        const Cx<RG>* sd = su + plane_s;
         Stg<R> dv[DD];
         Stg<R> sv[NS];
         // all loads of the walker are issued before any math (memory-level parallelism)
 #pragma unroll
-        for (int d = 0; d < DD; ++d) dv[d] = ld_stg_v(su + offd[d], sd + offd[d]);
+        for (int d = 0; d < DD; ++d) dv[d] = widen<R>(ld_stg_v(su + offd[d], sd + offd[d]));
 #pragma unroll
-        for (int j = 0; j < NS; ++j) sv[j] = ld_stg_v(su + offs[j], sd + offs[j]);
+        for (int j = 0; j < NS; ++j) sv[j] = widen<R>(ld_stg_v(su + offs[j], sd + offs[j]));
 #pragma unroll
         for (int p = 0; p < PP; ++p) {
 #pragma unroll
@@ -212,13 +224,13 @@ k_accumulate(const __grid_constant__ AccParams<R> P) {
             if (okmask & (1u << (p * DD + d))) st_g4(gb + p * nn + offg[d], acc[p][d]);
 }
 
-template <typename R, int PP, int DD, int WARPS, int MINB, bool FUSED>
-static g4_status launch_v1(const AccParams<R>& prm, cudaStream_t st) {
+template <typename R, typename RG, int PP, int DD, int WARPS, int MINB, bool FUSED>
+static g4_status launch_v1(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int n = prm.n;
     const int64_t nx = (prm.hi - prm.lo + PP * WARPS - 1) / (PP * WARPS);
     const uint64_t ctas = (uint64_t)nx * ((n + 31) / 32) * ((n + DD - 1) / DD);
     if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
-    k_accumulate<R, PP, DD, WARPS, MINB, FUSED><<<(unsigned)ctas, dim3(32, WARPS), 0, st>>>(prm);
+    k_accumulate<R, RG, PP, DD, WARPS, MINB, FUSED><<<(unsigned)ctas, dim3(32, WARPS), 0, st>>>(prm);
     return check_cuda(cudaGetLastError(), "k_accumulate launch");
 }
 
@@ -316,7 +328,7 @@ __device__ __forceinline__ Stg<float> lds_plain(const Cx<float>* u, const Cx<flo
     return v;
 }
 
-template <typename R, class G, bool FUSED, int MINB>
+template <typename R, typename RG, class G, bool FUSED, int MINB>
 __global__ void __launch_bounds__(32 * G::CW, MINB)
 k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     constexpr int PP = G::PP, DD = G::DD, NST = G::NST;
@@ -393,16 +405,16 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     for (int w = 0; w < P.nbatch; ++w) {
         const int s = w % NST;
         mbar_wait(&full[s], (w / NST) & 1);
-        const Cx<R>* dir_u = reinterpret_cast<const Cx<R>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
-        const Cx<R>* dir_d = dir_u + G::DIR_ELEMS;
-        const Cx<R>* sh_u = reinterpret_cast<const Cx<R>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
-        const Cx<R>* sh_d = sh_u + G::SH_ELEMS;
+        const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
+        const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
+        const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
+        const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
         // Direct elements first (sheared box: row d, column lane); shifted elements
         // stream diagonal by diagonal (j = p - d + DD-1), one ahead.
         Stg<R> dv[DD];
 #pragma unroll
-        for (int d = 0; d < DD; ++d) dv[d] = lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o);
-        Stg<R> snext = lds_plain(sh_u + sh_o, sh_d + sh_o);
+        for (int d = 0; d < DD; ++d) dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
+        Stg<R> snext = widen<R>(lds_plain(sh_u + sh_o, sh_d + sh_o));
         // Producer duty (lane 0 of warp 0): refill the stage every warp released in
         // the previous iteration with walker w - 1 + NST; its TMA overlaps this math.
         if (producer && w >= 1 && w - 1 + NST < P.nbatch) {
@@ -414,7 +426,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         for (int j = 0; j < PP + DD - 1; ++j) {
             const Stg<R> S = snext;
             if (j + 1 < PP + DD - 1)
-                snext = lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W);
+                snext = widen<R>(lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W));
 #pragma unroll
             for (int d = 0; d < DD; ++d) {
                 const int p = j + d - (DD - 1);
@@ -511,11 +523,11 @@ static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, Ma
     return G4_OK;
 }
 
-template <typename R, class G, bool FUSED, int MINB>
-static g4_status launch_v2(const AccParams<R>& prm, cudaStream_t st) {
+template <typename R, typename RG, class G, bool FUSED, int MINB>
+static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
-        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, G, FUSED, MINB>,
+        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
         attr_set = true;
     }
@@ -539,7 +551,7 @@ static g4_status launch_v2(const AccParams<R>& prm, cudaStream_t st) {
         tp.nx = (int32_t)((planes + G::PP * G::CW - 1) / (G::PP * G::CW));
         const uint64_t ctas = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DD - 1) / G::DD);
         if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
-        k_accumulate_tma<R, G, FUSED, MINB><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
+        k_accumulate_tma<R, RG, G, FUSED, MINB><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
         G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
     }
     return G4_OK;
@@ -557,42 +569,42 @@ static int v2_geom() {
     return g;
 }
 
-template <typename R, bool FUSED>
-static g4_status launch_v2_auto(const AccParams<R>& prm, cudaStream_t st) {
+template <typename R, typename RG, bool FUSED>
+static g4_status launch_v2_auto(const AccParams<R, RG>& prm, cudaStream_t st) {
     switch (v2_geom()) {
-        case 0: return launch_v2<R, V2Geom<R, 4, 4, 3>, FUSED, 3>(prm, st);
-        case 1: return launch_v2<R, V2Geom<R, 8, 2, 3>, FUSED, 3>(prm, st);
-        case 2: return launch_v2<R, V2Geom<R, 8, 4, 2>, FUSED, 2>(prm, st);
-        default: return launch_v2<R, V2Geom<R, 4, 4, 2>, FUSED, 4>(prm, st);
+        case 0: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3>, FUSED, 3>(prm, st);
+        case 1: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3>, FUSED, 3>(prm, st);
+        case 2: return launch_v2<R, RG, V2Geom<RG, 8, 4, 2>, FUSED, 2>(prm, st);
+        default: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
     }
 }
 
 // ---------------------------------------------------------------------------
-template <typename R, bool FUSED>
-static g4_status dispatch_t(const AccParams<R>& prm, cudaStream_t st) {
+template <typename R, typename RG, bool FUSED>
+static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     const int variant = kernel_variant();
-    if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2_auto<R, FUSED>(prm, st);
-    if (variant == 2 && prm.n >= 64) return launch_v2_auto<R, FUSED>(prm, st);
-    if (planes <= 4) return launch_v1<R, 4, 4, 1, 12, FUSED>(prm, st);
-    if (planes <= 8) return launch_v1<R, 4, 4, 2, 6, FUSED>(prm, st);
-    return launch_v1<R, 4, 4, 4, 3, FUSED>(prm, st);
+    if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2_auto<R, RG, FUSED>(prm, st);
+    if (variant == 2 && prm.n >= 64) return launch_v2_auto<R, RG, FUSED>(prm, st);
+    if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
+    if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
+    return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
 }
 
 static int g_arith = G4_ARITH_EXACT;
 
-template <typename R>
-static g4_status dispatch(const AccParams<R>& prm, cudaStream_t st) {
-    return g_arith == G4_ARITH_FUSED ? dispatch_t<R, true>(prm, st) : dispatch_t<R, false>(prm, st);
+template <typename R, typename RG>
+static g4_status dispatch(const AccParams<R, RG>& prm, cudaStream_t st) {
+    return g_arith == G4_ARITH_FUSED ? dispatch_t<R, RG, true>(prm, st) : dispatch_t<R, RG, false>(prm, st);
 }
 
-template <typename R>
+template <typename R, typename RG>
 static g4_status accumulate_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                               int32_t nbatch, cudaStream_t st) {
     if (!aligned(g4p, sizeof(Cx<R>)))
         return fail(G4_ERR_CONTRACT, "accumulate: g4 slice pointer is not entry-aligned");
     for (int32_t b0 = 0; b0 < nbatch; b0 += G4_MAX_BATCH) {
-        AccParams<R> prm{};
+        AccParams<R, RG> prm{};
         prm.g4 = static_cast<Cx<R>*>(g4p);
         prm.lo = lo;
         prm.hi = hi;
@@ -602,7 +614,7 @@ static g4_status accumulate_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
             const void* sp = staged[b0 + i];
             if (!sp) return fail(G4_ERR_CONTRACT, "accumulate: null staged payload");
             if (!aligned(sp, 16)) return fail(G4_ERR_CONTRACT, "accumulate: staged payload is not 16-B aligned");
-            prm.stg[i] = static_cast<const Cx<R>*>(sp);
+            prm.stg[i] = static_cast<const Cx<RG>*>(sp);
         }
         G4_TRY(dispatch(prm, st));
     }
@@ -627,8 +639,9 @@ g4_status g4_accumulate_staged(void* g4p, int64_t lo, int64_t hi, int32_t n, con
     if (nbatch == 0) return G4_OK;
     if (!g4p || !staged) return fail(G4_ERR_CONTRACT, "accumulate: null pointer");
     auto st = static_cast<cudaStream_t>(stream);
-    if (dtype == G4_C128) return accumulate_t<double>(g4p, lo, hi, n, staged, nbatch, st);
-    if (dtype == G4_C64) return accumulate_t<float>(g4p, lo, hi, n, staged, nbatch, st);
+    if (dtype == G4_C128) return accumulate_t<double, double>(g4p, lo, hi, n, staged, nbatch, st);
+    if (dtype == G4_C64) return accumulate_t<float, float>(g4p, lo, hi, n, staged, nbatch, st);
+    if (dtype == G4_C128_G64) return accumulate_t<double, float>(g4p, lo, hi, n, staged, nbatch, st);
     return fail(G4_ERR_CONTRACT, "unknown dtype");
 }
 
@@ -666,7 +679,9 @@ g4_status g4_accumulate(void* g4p, int64_t lo, int64_t hi, int32_t n, const void
     for (int32_t b0 = 0; b0 < nbatch; b0 += G4_MAX_BATCH) {
         const int32_t nb = std::min<int32_t>(G4_MAX_BATCH, nbatch - b0);
         for (int i = 0; i < nb; ++i) stg[i] = static_cast<char*>(workspace) + i * pb;
-        G4_TRY(g4_prepare_g(stg, up + b0, down + b0, nb, n, dtype, dtype, stream));
+        const int32_t din = dtype == G4_C128_G64 ? G4_C128 : dtype;   // reference-layout input type
+        const int32_t dout = dtype == G4_C128_G64 ? G4_C64 : dtype;   // staged payload type
+        G4_TRY(g4_prepare_g(stg, up + b0, down + b0, nb, n, din, dout, stream));
         G4_TRY(g4_accumulate_staged(g4p, lo, hi, n, stg, nb, dtype, channel, stream));
     }
     return G4_OK;

@@ -27,12 +27,13 @@ const char* g4_last_error(void) { return g4::t_err; }
 int32_t g4_abi_version(void) { return G4RING_ABI_VERSION; }
 
 int64_t g4_payload_bytes(int32_t n, int32_t dtype) {
-    if (n < 1 || (dtype != G4_C128 && dtype != G4_C64)) return -1;
+    // G4_C128_G64 payloads are complex64
+    if (n < 1 || (dtype != G4_C128 && dtype != G4_C64 && dtype != G4_C128_G64)) return -1;
     return 2 * g4::staged_plane(n, (int)g4::entry_bytes(dtype)) * g4::entry_bytes(dtype);
 }
 
 g4_status g4_staged_dims(int32_t n, int32_t dtype, int32_t* rows, int32_t* ld) {
-    if (n < 1 || !rows || !ld || (dtype != G4_C128 && dtype != G4_C64))
+    if (n < 1 || !rows || !ld || (dtype != G4_C128 && dtype != G4_C64 && dtype != G4_C128_G64))
         return g4::fail(G4_ERR_CONTRACT, "staged_dims: bad arguments");
     *rows = g4::staged_rows(n, (int)g4::entry_bytes(dtype));
     *ld = g4::staged_ld(n, (int)g4::entry_bytes(dtype));

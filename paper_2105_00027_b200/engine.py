@@ -38,8 +38,8 @@ from . import _lib
 from . import schedule as S
 from .errors import ConfigError, ContractViolation, DeadlockError
 from .schedule import LaneRing, RingTopology, lane_ring_id  # noqa: F401  (re-exported API)
-from .tensor import (CombinedIndexSpace, GtSlice, Origin, _dtype_code, make_partition,
-                     staged_shape)
+from .tensor import (CombinedIndexSpace, GtSlice, Origin, _dtype_code, accumulate_dtype_code,
+                     make_partition, staged_shape)
 
 VALUE_MODES = ("float", "integer")
 _MODE_CODE = {"float": _lib.G4_MODE_FLOAT, "integer": _lib.G4_MODE_INTEGER}
@@ -64,7 +64,7 @@ class ExperimentConfig:
     # B200 extensions
     planes: int | None = None      # exchange planes K3 in [0, planes); None = all N (reference)
     batch: int = 1                 # measurements per lane carried by one ring message / K1 pass
-    dtype: str = "c128"            # "c128" (reference) or "c64"
+    dtype: str = "c128"            # "c128" (reference), "c64", or "c128g64" (c128 G4, c64 payloads)
     gather: bool = True            # assemble the full tensor on world rank 0
     # test hooks (never part of a user config, as in the reference)
     ring_steps_override: int | None = None
@@ -103,8 +103,8 @@ def validate_config(cfg: ExperimentConfig) -> None:
         raise ConfigError(f"value_mode must be one of {VALUE_MODES}, got {cfg.value_mode!r}")
     if cfg.direction not in ("forward", "alternate"):
         raise ConfigError(f"direction must be forward or alternate, got {cfg.direction!r}")
-    if cfg.dtype not in ("c128", "c64"):
-        raise ConfigError(f"dtype must be c128 or c64, got {cfg.dtype!r}")
+    if cfg.dtype not in ("c128", "c64", "c128g64"):
+        raise ConfigError(f"dtype must be c128, c64 or c128g64, got {cfg.dtype!r}")
     if cfg.timeout_s <= 0:
         raise ConfigError("timeout_s must be positive")
 
@@ -250,15 +250,17 @@ class RingEngine:
         self.space = CombinedIndexSpace(cfg.n_k, cfg.n_w)
         n = self.space.size
         self.lo, self.hi = make_partition(cfg.num_planes, cfg.subring_size).ranges[self.pos]
-        self.dtype = torch.complex128 if cfg.dtype == "c128" else torch.complex64
-        self.code = _dtype_code(self.dtype)
+        self.dtype = torch.complex64 if cfg.dtype == "c64" else torch.complex128         # G4 slice
+        self.pdtype = torch.complex128 if cfg.dtype == "c128" else torch.complex64       # payloads
+        self.code = accumulate_dtype_code(self.dtype, self.pdtype)
+        self.pcode = _dtype_code(self.pdtype)
         self.slice = GtSlice.zeros(self.space, self.lo, self.hi, device=device, dtype=self.dtype)
         self.channels = S.make_channels(self.topo, self.pos)
         self.lib = _lib.load()
         # per channel: 3 buffers (GEN, R0, R1) x batch x lanes staged payloads
-        self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n, self.dtype), dtype=self.dtype,
+        self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n, self.pdtype), dtype=self.pdtype,
                                  device=device) for c in self.channels]
-        self.payload_bytes = int(np.prod(staged_shape(n, self.dtype))) * self.bufs[0].element_size()
+        self.payload_bytes = int(np.prod(staged_shape(n, self.pdtype))) * self.bufs[0].element_size()
         self.flags = torch.zeros(len(self.channels) * S.FLAGS_PER_CHANNEL, dtype=torch.int64, device=device)
         self.compute = torch.cuda.Stream(device)
         self.comm = [torch.cuda.Stream(device) for _ in self.channels]
@@ -344,7 +346,7 @@ class RingEngine:
                 _lib.check(lib.g4_generate(_lib.ptr_array(ptrs), None, None, len(ptrs),
                                            cfg.seed & 0xFFFFFFFFFFFFFFFF, _lib.i64_array(wr),
                                            _lib.i64_array(lanes), _lib.i64_array(meas), self.space.size,
-                                           _MODE_CODE[cfg.value_mode], self.code, self.compute.cuda_stream),
+                                           _MODE_CODE[cfg.value_mode], self.pcode, self.compute.cuda_stream),
                            "generate")
             elif kind == "acc":
                 ptrs = []
@@ -413,7 +415,7 @@ class RingEngine:
         code_in = _dtype_code(ups[0].dtype)
         _lib.check(self.lib.g4_prepare_g(_lib.ptr_array(ptrs), _lib.ptr_array([u.data_ptr() for u in ups]),
                                          _lib.ptr_array([d.data_ptr() for d in downs]), len(ptrs),
-                                         self.space.size, code_in, self.code, self.compute.cuda_stream),
+                                         self.space.size, code_in, self.pcode, self.compute.cuda_stream),
                    "prepare_g")
 
     def rounds(self) -> int:

@@ -324,20 +324,32 @@ def accumulate_g4_batch(slice_: GtSlice, gs: list[GSigma]) -> None:
     Bitwise identical to calling ``accumulate_g4`` on each payload in order."""
     if not gs:
         return
+    pdt = gs[0].staged.dtype
     for g in gs:
         if g.space != slice_.space:
             raise ContractViolation(f"space mismatch: slice {slice_.space} vs payload {g.space}")
-        if g.staged.dtype != slice_.data.dtype:
-            raise ContractViolation(f"payload dtype {g.staged.dtype} != slice dtype {slice_.data.dtype}")
+        if g.staged.dtype != pdt:
+            raise ContractViolation("all payloads of a batch must share a dtype")
         if g.staged.device != slice_.data.device:
             raise ContractViolation("payload and slice live on different devices")
+    code = accumulate_dtype_code(slice_.data.dtype, pdt)
     lib = _lib.load()
     dev = slice_.data.device
     _lib.check(lib.g4_accumulate_staged(
         slice_.data.data_ptr(), slice_.lo, slice_.hi, slice_.space.size,
-        _lib.ptr_array([g.staged.data_ptr() for g in gs]), len(gs), _dtype_code(slice_.data.dtype),
+        _lib.ptr_array([g.staged.data_ptr() for g in gs]), len(gs), code,
         _lib.G4_CHANNEL_EQ1, _stream_ptr(dev)), "accumulate_g4")
     slice_.meas_count += len(gs)
+
+
+def accumulate_dtype_code(slice_dtype: torch.dtype, payload_dtype: torch.dtype) -> int:
+    """C-ABI dtype of an update: same precision, or the mixed complex128 slice /
+    complex64 payload mode (G4_C128_G64)."""
+    if slice_dtype == payload_dtype:
+        return _dtype_code(slice_dtype)
+    if slice_dtype == torch.complex128 and payload_dtype == torch.complex64:
+        return _lib.G4_C128_G64
+    raise ContractViolation(f"payload dtype {payload_dtype} cannot update a {slice_dtype} slice")
 
 
 def accumulate_g4(slice_: GtSlice, g: GSigma) -> None:

@@ -91,6 +91,16 @@ def test_c64_ring_within_tolerance():
     assert O.compare(ref, rep.tensor.astype(np.complex128))["l2_real"] < 1e-5
 
 
+def test_mixed_precision_ring():
+    c = cfg(world_size=2, subring_size=2, lanes=2, measurements=2, value_mode="float", dtype="c128g64",
+            n_k=4, n_w=24, planes=40)
+    rep = E.run_experiment(c)
+    assert rep.tensor.dtype == np.complex128
+    ref = oracle_of(c)
+    r = O.compare(ref, rep.tensor)
+    assert max(r["l1_real"], r["l1_imag"], r["l2_real"], r["l2_imag"]) < 1e-6  # c64-rounded payloads
+
+
 def test_short_ring_negative_control():
     c = cfg(world_size=3, subring_size=3, n_w=3, ring_steps_override=1)
     rep = E.run_experiment(c)

@@ -325,3 +325,28 @@ def test_fused_arith_within_tolerance(oracle, cuda_dev, variant):
     finally:
         _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
         _lib.check(lib.g4_set_kernel_variant(0))
+
+
+@pytest.mark.parametrize("n,lo,hi,variant", [(40, 3, 9, 0), (128, 0, 40, 0), (128, 0, 40, 1), (161, 150, 161, 2)])
+def test_mixed_precision_bitwise(oracle, cuda_dev, n, lo, hi, variant):
+    """complex128 G4 with complex64 payloads: bitwise equal to the complex128
+    reference applied to the complex64-rounded payloads (widening is exact)."""
+    lib = _lib.load()
+    _lib.check(lib.g4_set_kernel_variant(variant))
+    try:
+        rng = np.random.default_rng(n)
+        sp = T.CombinedIndexSpace(1, n)
+        start = rng.standard_normal((hi - lo, n, n)) + 1j * rng.standard_normal((hi - lo, n, n))
+        ref = start.copy()
+        sl = T.GtSlice(sp, lo, hi, torch.from_numpy(start).to(cuda_dev))
+        gs = []
+        for _ in range(5):
+            up = (rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n)))
+            down = (rng.uniform(-1, 1, (n, n)) + 1j * rng.uniform(-1, 1, (n, n)))
+            gs.append(T.GSigma(sp, up, down, device=cuda_dev, dtype=torch.complex64))  # K2 rounds c128 -> c64
+            oracle.accumulate(ref, lo, hi, up.astype(np.complex64).astype(np.complex128),
+                              down.astype(np.complex64).astype(np.complex128))
+        T.accumulate_g4_batch(sl, gs)
+        assert np.array_equal(to_np(sl.data), ref)
+    finally:
+        _lib.check(lib.g4_set_kernel_variant(0))
