@@ -299,6 +299,7 @@ def run_gpu(args):
         "e2e": e2e,
         "gpu_launches": args.steps,
         "g4_bytes": sl.nbytes,
+        "max_g4": max_g4_capacity(dev, walkers=B),
     }
     if not args.no_cpu_baseline:
         from oracle import oracle as O
@@ -309,6 +310,57 @@ def run_gpu(args):
             "sample": f"{max(2, args.cpu_steps)} steps of {B} walkers x {planes} planes x N^2={n * n}, "
                       f"numpy port of accumulate_g4 in {used} processes on disjoint K3 ranges; "
                       f"host {cpu_model()}"}
+    print(json.dumps(line), flush=True)
+
+
+def max_g4_capacity(dev, n=4608, walkers=8, margin=6e9):
+    """Largest complex128 G4 slice (planes of N x N) that fits next to `walkers`
+    staged payloads on this GPU; and the 8-GPU total (BASELINE config 4 scale)."""
+    import torch
+    from paper_2105_00027_b200 import tensor as T
+    free, total = torch.cuda.mem_get_info(dev)
+    payload = 2 * int(__import__("numpy").prod(T.staged_shape(n)[1:])) * 16
+    plane = n * n * 16
+    planes = int((free - walkers * payload - margin) // plane)
+    return {"n": n, "planes_per_gpu": planes, "bytes_per_gpu": planes * plane,
+            "bytes_8gpu": 8 * planes * plane, "gpu_free_bytes": free, "gpu_total_bytes": total,
+            "config4_bytes": 576 * plane}
+
+
+def run_max_g4(args):
+    """--max-g4: allocate the largest N=4608 complex128 slice that fits this GPU,
+    apply one device-generated walker in one K1 pass, verify the first and last
+    planes against the C oracle (test infrastructure, host)."""
+    import numpy as np
+    import torch
+    from oracle import oracle as O
+    from paper_2105_00027_b200 import tensor as T
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    cap = max_g4_capacity(dev, walkers=1)
+    sp = T.CombinedIndexSpace(36, 128)
+    n = sp.size
+    planes = cap["planes_per_gpu"]
+    sl = T.GtSlice.zeros(sp, 0, planes, device=dev)
+    g = T.generate_gsigma(7, T.Origin(0, 0, 0, 0, 0), sp, "float", device=dev)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    T.accumulate_g4(sl, g)
+    t1.record()
+    torch.cuda.synchronize()
+    ms = t0.elapsed_time(t1)
+    up, down = O.gsigma(7, 0, 0, 0, n, "float")
+    checks = {}
+    for k3 in (0, planes - 1):
+        ref = np.zeros((1, n, n), np.complex128)
+        O.accumulate(ref, k3, k3 + 1, up, down)
+        got = sl.data[k3].cpu().numpy()
+        checks[k3] = float(np.abs(got - ref[0]).max() / np.abs(ref).max())
+    line = {"metric": "max G4 per GPU", "value": sl.nbytes, "unit": "bytes", "planes": planes, "n": n,
+            "dtype": "c128", "pass_ms": ms, "pass_gbs": 2 * sl.nbytes / (ms * 1e-3) / 1e9,
+            "verified_planes_max_rel_err": checks, "ok": all(v < 1e-10 for v in checks.values()),
+            "capacity": cap}
     print(json.dumps(line), flush=True)
 
 
@@ -530,12 +582,15 @@ def main():
                     help="exact: reference op order (bitwise); fused: FMA-chained (within 1e-10)")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--planes", type=int, default=0, help="override the exchange-plane count (N=1)")
+    ap.add_argument("--max-g4", action="store_true", help="allocate + update + verify the largest N=4608 slice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
     if args.impl == "reference":
         return run_reference(args)
+    if args.max_g4:
+        return run_max_g4(args)
     return run_gpu(args)
 
 

@@ -66,6 +66,7 @@ class ExperimentConfig:
     batch: int = 1                 # measurements per lane carried by one ring message / K1 pass
     dtype: str = "c128"            # "c128" (reference), "c64", or "c128g64" (c128 G4, c64 payloads)
     gather: bool = True            # assemble the full tensor on world rank 0
+    sample_planes: tuple[int, ...] = ()  # K3 planes copied to world rank 0 (report.samples)
     # test hooks (never part of a user config, as in the reference)
     ring_steps_override: int | None = None
     fault: str | None = None
@@ -472,6 +473,7 @@ class ExperimentReport:
     elapsed_s: float
     clock: str = "cuda-event"
     round_ms: dict[int, list[float]] = field(default_factory=dict)
+    samples: dict[int, np.ndarray] = field(default_factory=dict)
 
     def to_json_dict(self) -> dict:
         return {"config": self.config, "clock": self.clock, "elapsed_s": self.elapsed_s,
@@ -524,6 +526,7 @@ def rank_main(cfg: ExperimentConfig, world: Control | None = None) -> Experiment
     tensor = None
     if cfg.gather:
         tensor = _gather_full(world, eng, cfg)
+    samples = _gather_planes(world, eng, cfg, cfg.sample_planes) if cfg.sample_planes else {}
     blob = {"rank": r, "meas_count": eng.meas_count, "slice": [eng.lo, eng.hi],
             "counters": {t: c.to_dict() for t, c in eng.counters.items()},
             "origins": {t: eng.origins[t] for t in eng.origins},
@@ -546,7 +549,7 @@ def rank_main(cfg: ExperimentConfig, world: Control | None = None) -> Experiment
                                   "origins": [tuple(o) for o in b["origins"][t]]}
     return ExperimentReport(config=cfg.to_dict(), tensor=tensor, meas_counts=meas, lane_counters=counters,
                             lane_meta=meta, memory_peaks=peaks, slices=slices, elapsed_s=elapsed,
-                            round_ms=rms)
+                            round_ms=rms, samples=samples)
 
 
 def _gather_full(world: Control, eng: RingEngine, cfg: ExperimentConfig) -> np.ndarray | None:
@@ -570,6 +573,34 @@ def _gather_full(world: Control, eng: RingEngine, cfg: ExperimentConfig) -> np.n
         finally:
             pm.close()
         out = full.cpu().numpy()
+    world.barrier()
+    return out
+
+
+def _gather_planes(world: Control, eng: RingEngine, cfg: ExperimentConfig, planes) -> dict[int, np.ndarray]:
+    """Copy selected reduced K3 planes to world rank 0 without assembling the
+    whole tensor (for G4s far larger than one GPU)."""
+    s = cfg.subring_size
+    torch.cuda.synchronize(eng.device)
+    info = world.allgather((export_ptr(eng.slice.data.data_ptr()), eng.lo, eng.hi))
+    out = {}
+    if world.rank == 0:
+        n = eng.space.size
+        buf = torch.empty((n, n), dtype=eng.dtype, device=eng.device)
+        pm = PeerMap()
+        try:
+            for k3 in planes:
+                if not (0 <= k3 < cfg.num_planes):
+                    raise ContractViolation(f"sample plane {k3} outside [0, {cfg.num_planes})")
+                q = next(i for i in range(s) if info[i][1] <= k3 < info[i][2])
+                (h, off), lo, _ = info[q]
+                ptr = pm.open(h, off, eng.slice.data.data_ptr() if q == 0 else None)
+                nbytes = n * n * buf.element_size()
+                _lib.check(eng.lib.g4_copy_async(buf.data_ptr(), ptr + (k3 - lo) * nbytes, nbytes,
+                                                 torch.cuda.current_stream(eng.device).cuda_stream), "sample")
+                out[k3] = buf.cpu().numpy().copy()
+        finally:
+            pm.close()
     world.barrier()
     return out
 

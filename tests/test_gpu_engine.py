@@ -101,6 +101,23 @@ def test_mixed_precision_ring():
     assert max(r["l1_real"], r["l1_imag"], r["l2_real"], r["l2_imag"]) < 1e-6  # c64-rounded payloads
 
 
+def test_config4_scale_distributed_sampled_planes(oracle):
+    """BASELINE config 4 index space (N = 4608): 2 ranks x 72 planes (the per-GPU
+    share of the 8-GPU run, 49 GB of G4 in total) accumulated through the ring
+    without gathering; sampled planes (first/last of each slice) vs the C oracle."""
+    c = cfg(n_k=36, n_w=128, world_size=2, subring_size=2, lanes=1, measurements=1, value_mode="float",
+            planes=144, gather=False, sample_planes=(0, 71, 72, 143), timeout_s=120.0, seed=3)
+    rep = E.run_experiment(c)
+    assert rep.tensor is None and set(rep.samples) == {0, 71, 72, 143}
+    n = 4608
+    walkers = [oracle.gsigma(c.seed, wr, 0, 0, n, "float") for wr in range(2)]
+    for k3, got in rep.samples.items():
+        ref = np.zeros((1, n, n), np.complex128)
+        for up, down in walkers:
+            oracle.accumulate(ref, k3, k3 + 1, up, down)
+        np.testing.assert_allclose(got, ref[0], rtol=1e-10, atol=1e-13)
+
+
 def test_short_ring_negative_control():
     c = cfg(world_size=3, subring_size=3, n_w=3, ring_steps_override=1)
     rep = E.run_experiment(c)
