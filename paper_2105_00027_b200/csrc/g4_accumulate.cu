@@ -272,9 +272,9 @@ constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel 
 
 // Geometry of one v2 configuration: PP planes x DD diagonal entries per thread,
 // CW warps stacked along K3 per CTA, NST-stage shared-memory ring, entry type R.
-template <typename R, int PP_, int CW_, int NST_>
+template <typename R, int PP_, int CW_, int NST_, int DD_ = 4>
 struct V2Geom {
-    static constexpr int PP = PP_, DD = 4, CW = CW_, NST = NST_;
+    static constexpr int PP = PP_, DD = DD_, CW = CW_, NST = NST_;
     static constexpr int ES = sizeof(Cx<R>);                      // bytes per complex entry
     static constexpr int NSH = PP * CW + DD - 1;                  // shifted row segments (band height)
     // Box row width in entries.  A TMA box must start on a 16-B boundary along
@@ -470,7 +470,7 @@ struct MapPair {
 // is non-negative, and the map's base (stg - off * es) stays 16-B aligned.
 static int sheared_offset(int n, int es) { return (es == 8 && (n & 1)) ? n + 1 : n; }
 
-static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, MapPair* out) {
+static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, int dd, MapPair* out) {
     static PFN_encodeTiled encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
@@ -494,7 +494,7 @@ static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, M
     const cuuint32_t estr[3] = {1, 1, 1};
     void* base = static_cast<char*>(const_cast<void*>(stg)) - (size_t)off * es;
     for (int which = 0; which < 2; ++which) {
-        const cuuint32_t box[3] = {(cuuint32_t)width * ew, which == 0 ? 4u : (cuuint32_t)nsh, 2};
+        const cuuint32_t box[3] = {(cuuint32_t)width * ew, which == 0 ? (cuuint32_t)dd : (cuuint32_t)nsh, 2};
         CUresult r = encode(which == 0 ? &out->dmap : &out->smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base,
                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -507,17 +507,17 @@ static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, M
     return G4_OK;
 }
 
-static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, MapPair* out) {
+static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, int dd, MapPair* out) {
     static std::mutex mu;
-    static std::map<std::tuple<uintptr_t, int, int, int>, MapPair> cache;
-    const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(stg), n, nsh, es);
+    static std::map<std::tuple<uintptr_t, int, int, int, int>, MapPair> cache;
+    const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(stg), n, nsh, es, dd);
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it != cache.end()) {
         *out = it->second;
         return G4_OK;
     }
-    G4_TRY(make_maps(stg, n, es, nsh, width, out));
+    G4_TRY(make_maps(stg, n, es, nsh, width, dd, out));
     if (cache.size() > 4096) cache.clear();
     cache.emplace(key, *out);
     return G4_OK;
@@ -543,7 +543,7 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
-            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, &mp));
+            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, G::DD, &mp));
             tp.dmap[i] = mp.dmap;
             tp.smap[i] = mp.smap;
         }
@@ -575,6 +575,9 @@ static g4_status launch_v2_auto(const AccParams<R, RG>& prm, cudaStream_t st) {
         case 0: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3>, FUSED, 3>(prm, st);
         case 1: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3>, FUSED, 3>(prm, st);
         case 2: return launch_v2<R, RG, V2Geom<RG, 8, 4, 2>, FUSED, 2>(prm, st);
+        case 4: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 2>, FUSED, 6>(prm, st);
+        case 5: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 3>, FUSED, 5>(prm, st);
+        case 6: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 2>, FUSED, 5>(prm, st);
         default: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
     }
 }
