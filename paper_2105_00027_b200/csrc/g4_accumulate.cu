@@ -270,19 +270,26 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
 }
 constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel params)
 
-// Geometry of one v2 configuration: PP planes x DD diagonal entries per thread,
-// CW warps stacked along K3 per CTA, NST-stage shared-memory ring, entry type R.
-template <typename R, int PP_, int CW_, int NST_, int DD_ = 4>
+// Geometry of one v2 configuration.  A thread owns PP planes x DD diagonal
+// entries; a CTA is CWQ x CWR warps: CWQ stacked along K3 (Q = PP*CWQ planes)
+// and CWR along the diagonal (DR = DD*CWR entries per lane, i.e. the CTA's
+// G4 tile is Q planes x the 32-wide diagonal strip (k1_0 + e, j0 + lane + e),
+// e < DR).  Per walker the CTA fetches DR direct rows and Q + DR - 1 band rows
+// (32 entries x 2 spins each): (Q + 2 DR - 1) / (Q DR) rows per G4 entry.
+// NST-stage shared-memory ring, payload entry type R.
+template <typename R, int PP_, int CW_, int NST_, int DD_ = 4, int CWR_ = 1>
 struct V2Geom {
-    static constexpr int PP = PP_, DD = DD_, CW = CW_, NST = NST_;
+    static constexpr int PP = PP_, DD = DD_, CWQ = CW_, CWR = CWR_, NST = NST_;
+    static constexpr int CW = CWQ * CWR;                          // warps per CTA
+    static constexpr int Q = PP * CWQ, DR = DD * CWR;             // CTA tile: planes x diagonal entries
     static constexpr int ES = sizeof(Cx<R>);                      // bytes per complex entry
-    static constexpr int NSH = PP * CW + DD - 1;                  // shifted row segments (band height)
+    static constexpr int NSH = Q + DR - 1;                        // shifted row segments (band height)
     // Box row width in entries.  A TMA box must start on a 16-B boundary along
     // its innermost dimension (tools/tma_probe.cu: odd 8-B starts fault), so for
     // complex64 boxes start at the even entry below and carry 2 extra entries;
     // consumers add the start's parity (0 or 1).
     static constexpr int W = ES == 8 ? 34 : 32;
-    static constexpr int DIR_ELEMS = DD * W;                      // per spin (sheared direct box)
+    static constexpr int DIR_ELEMS = DR * W;                      // per spin (sheared direct box)
     static constexpr int SH_ELEMS = NSH * W;                      // per spin
     static constexpr uint32_t DIR_BYTES = 2 * DIR_ELEMS * ES;     // both spins
     static constexpr uint32_t SH_BYTES = 2 * SH_ELEMS * ES;
@@ -291,6 +298,7 @@ struct V2Geom {
     static constexpr uint32_t STAGE_BYTES = (SH_OFF + SH_BYTES + 127) / 128 * 128;
     static constexpr size_t SMEM = (size_t)NST * STAGE_BYTES + 2 * NST * sizeof(uint64_t);
     static_assert(NSH <= G4_HALO_ROWS && NSH + W + 1 < G4_HALO_COLS, "halo too small for the v2 band");
+    static_assert(SMEM <= 227 * 1024, "v2 stages exceed shared memory");
 };
 
 template <typename R>
@@ -303,7 +311,22 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
     int32_t nx;   // plane chunks
     int32_t off;  // sheared-coordinate offset (elements), see make_maps
+    int32_t ahead;  // CTAs resident on the whole GPU (L2 prefetch distance)
 };
+
+// Measurement-only variants of K1 v2 (G4RING_EXP, never set in production):
+//   1 = start from zero accumulators (no G4 read)   2 = no G4 write
+//   4 = no shared-memory reads / math                8 = L2-prefetch the G4 tile
+//       of the CTA one resident wave ahead
+enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, EXP_PREFETCH = 8 };
+static int exp_flags() {
+    static int e = -1;
+    if (e < 0) {
+        const char* v = getenv("G4RING_EXP");
+        e = v ? atoi(v) : 0;
+    }
+    return e;
+}
 
 // Plain shared-memory loads the scheduler may move (ordered after the stage's
 // mbarrier wait by that asm's memory clobber).
@@ -328,7 +351,7 @@ __device__ __forceinline__ Stg<float> lds_plain(const Cx<float>* u, const Cx<flo
     return v;
 }
 
-template <typename R, typename RG, class G, bool FUSED, int MINB>
+template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
 __global__ void __launch_bounds__(32 * G::CW, MINB)
 k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     constexpr int PP = G::PP, DD = G::DD, NST = G::NST;
@@ -339,17 +362,18 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
 
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const TileCoord tc = tile_coord(blockIdx.x, P.nx, (n + 31) / 32, (n + DD - 1) / DD);
-    const int64_t q0 = P.lo + (int64_t)tc.x * (PP * G::CW);
+    constexpr int DR = G::DR, Q = G::Q;
+    const TileCoord tc = tile_coord(blockIdx.x, P.nx, (n + 31) / 32, (n + DR - 1) / DR);
+    const int64_t q0 = P.lo + (int64_t)tc.x * Q;
     const int j0 = tc.y * 32;
-    const int k1_0 = tc.z * DD;
+    const int k1_0 = tc.z * DR;
     const bool producer = threadIdx.x == 0;
     // Sheared coordinates (c1, c2) address stg[c2][c1 - off + c2].
     //  direct tile: rows k1_0 + i, columns j0 + i + j      -> (j0 - k1_0 + off, k1_0)
     //  shifted band: rows R0 + i, columns C0 + i + j with
-    //    R0 = (q0 - k1_0 - (DD-1)) mod N, C0 = (q0 - j0 - 31 - (DD-1)) mod N  -> (C0 - R0 + off, R0)
-    const int R0 = wrap((int)(q0 - k1_0) - (DD - 1), n);
-    const int C0 = wrap((int)(q0 - j0) - 31 - (DD - 1), n);
+    //    R0 = (q0 - k1_0 - (DR-1)) mod N, C0 = (q0 - j0 - 31 - (DR-1)) mod N  -> (C0 - R0 + off, R0)
+    const int R0 = wrap((int)(q0 - k1_0) - (DR - 1), n);
+    const int C0 = wrap((int)(q0 - j0) - 31 - (DR - 1), n);
     const int xd = j0 - k1_0 + P.off, xs = C0 - R0 + P.off;  // box starts (entries, >= 0)
     const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;  // 16-B alignment shift
     auto issue = [&](int w) {  // producer lane: both tensor boxes of walker w into stage w % NST
@@ -368,29 +392,52 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int w = 0; w < NST && w < P.nbatch; ++w) issue(w);
     }
+    if constexpr ((EXP & EXP_PREFETCH) != 0) {
+        // warp 1: the G4 rows of the CTA one resident wave ahead -> L2
+        const unsigned nb = blockIdx.x + (unsigned)P.ahead;
+        if (warp == 1 && nb < gridDim.x) {
+            const TileCoord t2 = tile_coord(nb, P.nx, (n + 31) / 32, (n + DR - 1) / DR);
+            const int64_t qa = P.lo + (int64_t)t2.x * Q;
+#pragma unroll 1
+            for (int i = 0; i < (Q * DR + 31) / 32; ++i) {
+                const int r = lane + 32 * i;  // (plane, row) pair
+                const int64_t q = qa + r / DR;
+                const int k1 = t2.z * DR + r % DR;
+                if (r < Q * DR && q < P.hi && k1 < n) {
+                    const int c0 = t2.y * 32 + r % DR;
+                    const int len = min(32, n - c0);
+                    const Cx<R>* a = P.g4 + ((q - P.lo) * n + k1) * (int64_t)n + c0;
+                    const uint32_t bytes = (uint32_t)(len * sizeof(Cx<R>)) & ~15u;
+                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+                }
+            }
+        }
+    }
     __syncthreads();
 
-    // ------------- warp w owns planes q0 + PP*w .. q0 + PP*w + PP-1 -------------
+    // ---- warp (wq, wr) owns planes q0 + PP*wq + p and diagonal entries e = DD*wr + d ----
+    const int wq = warp % G::CWQ, wr = warp / G::CWQ;
     const int c = j0 + lane;
     const bool col_ok = c < n;
     const int64_t nn = (int64_t)n * n;
-    const int64_t qw = q0 + PP * warp;
+    const int64_t qw = q0 + PP * wq;
+    const int e0 = DD * wr;
     Cx<R>* gb = P.g4 + (qw - P.lo) * nn;
     int offg[DD];
 #pragma unroll
-    for (int d = 0; d < DD; ++d) offg[d] = wrap(k1_0 + d, n) * n + wrap(c + d, n);
+    for (int d = 0; d < DD; ++d) offg[d] = wrap(k1_0 + e0 + d, n) * n + wrap(c + e0 + d, n);
     uint32_t okmask = 0;
 #pragma unroll
     for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int d = 0; d < DD; ++d)
-            if (col_ok && (qw + p) < P.hi && (k1_0 + d) < n) okmask |= 1u << (p * DD + d);
+            if (col_ok && (qw + p) < P.hi && (k1_0 + e0 + d) < n) okmask |= 1u << (p * DD + d);
     Cx<R> acc[PP][DD];
 #pragma unroll
     for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int d = 0; d < DD; ++d) {
-            if (okmask & (1u << (p * DD + d))) {
+            if ((EXP & EXP_NOLOAD) == 0 && (okmask & (1u << (p * DD + d)))) {
                 acc[p][d] = ld_g4(gb + p * nn + offg[d]);
             } else {
                 acc[p][d].re = R(0);
@@ -399,8 +446,9 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         }
 
     // shared-memory element offsets (complex units) inside a stage
-    const int sh_o = (PP * warp) * G::W + (31 - lane) + ps;  // + j * W
-    const int dr_o = lane + pd;                               // + d * W
+    // band row of (p, d) relative to R0: PP*wq + p - (e0 + d) + DR - 1
+    const int sh_o = (PP * wq + DR - DD - e0) * G::W + (31 - lane) + ps;  // + j * W
+    const int dr_o = e0 * G::W + lane + pd;                                // + d * W
 #pragma unroll 1
     for (int w = 0; w < P.nbatch; ++w) {
         const int s = w % NST;
@@ -409,6 +457,15 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
         const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
         const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
+        if constexpr ((EXP & EXP_NOMATH) != 0) {
+            if (producer && w >= 1 && w - 1 + NST < P.nbatch) {
+                mbar_wait(&empty[(w - 1) % NST], ((w - 1) / NST) & 1);
+                issue(w - 1 + NST);
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+            continue;
+        }
         // Direct elements first (sheared box: row d, column lane); shifted elements
         // stream diagonal by diagonal (j = p - d + DD-1), one ahead.
         Stg<R> dv[DD];
@@ -453,7 +510,171 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int d = 0; d < DD; ++d)
-            if (okmask & (1u << (p * DD + d))) st_g4(gb + p * nn + offg[d], acc[p][d]);
+            if (okmask & (1u << (p * DD + d))) {
+                if ((EXP & EXP_NOSTORE) == 0 || acc[p][d].re == R(-1234.5)) st_g4(gb + p * nn + offg[d], acc[p][d]);
+            }
+}
+
+// ---------------------------------------------------------------------------
+// v3 -- persistent CTAs.  Same tile, operand staging and arithmetic as v2, but
+// each CTA walks tiles lin = blockIdx.x + t * gridDim.x (the L2-aware order)
+// and the shared-memory ring runs continuously over the flat item sequence
+// (tile, walker): the producer keeps NST - 1 payload boxes in flight across
+// tile boundaries, so a tile's first walker is already resident when its G4
+// block has been read.  The G4 rows of the CTA's next tile are prefetched into
+// L2 while the current tile computes.
+template <typename R, typename RG, class G, bool FUSED, int MINB>
+__global__ void __launch_bounds__(32 * G::CW, MINB)
+k_accumulate_pers(const __grid_constant__ TmaParams<R> P) {
+    constexpr int PP = G::PP, DD = G::DD, NST = G::NST, DR = G::DR, Q = G::Q;
+    constexpr int EW = G::ES / 8;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NST * G::STAGE_BYTES);
+    uint64_t* empty = full + NST;
+
+    const int n = P.n;
+    const int nb = P.nbatch;
+    const int ny = (n + 31) / 32, nz = (n + DR - 1) / DR;
+    const unsigned ntiles = (unsigned)P.nx * ny * nz;
+    if (blockIdx.x >= ntiles) return;
+    const unsigned my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
+    const unsigned items = my_tiles * (unsigned)nb;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool producer = threadIdx.x == 0;
+
+    // Tile geometry (see k_accumulate_tma): sheared box starts of the direct
+    // tile and the shifted band, with the 16-B parity shift for complex64.
+    struct TileBox {
+        int64_t q0;
+        int j0, k1_0, xd, xs, R0, pd, ps;
+    };
+    auto tile_box = [&](unsigned t) {
+        const TileCoord tc = tile_coord(blockIdx.x + t * gridDim.x, P.nx, ny, nz);
+        TileBox b;
+        b.q0 = P.lo + (int64_t)tc.x * Q;
+        b.j0 = tc.y * 32;
+        b.k1_0 = tc.z * DR;
+        b.R0 = wrap((int)(b.q0 - b.k1_0) - (DR - 1), n);
+        const int C0 = wrap((int)(b.q0 - b.j0) - 31 - (DR - 1), n);
+        b.xd = b.j0 - b.k1_0 + P.off;
+        b.xs = C0 - b.R0 + P.off;
+        b.pd = (G::ES == 8) ? (b.xd & 1) : 0;
+        b.ps = (G::ES == 8) ? (b.xs & 1) : 0;
+        return b;
+    };
+    auto issue = [&](unsigned k) {  // producer lane: item k = (tile k / nb, walker k % nb)
+        const int s = (int)(k % NST);
+        const unsigned t = k / (unsigned)nb;
+        const int w = (int)(k - t * (unsigned)nb);
+        const TileBox b = tile_box(t);
+        mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
+        unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
+        tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (b.xd - b.pd), b.k1_0, 0, &full[s]);
+        tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (b.xs - b.ps), b.R0, 0, &full[s]);
+    };
+    if (producer) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], G::CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (unsigned k = 0; k < (unsigned)NST && k < items; ++k) issue(k);
+    }
+    __syncthreads();
+
+    const int wq = warp % G::CWQ, wr = warp / G::CWQ;
+    const int e0 = DD * wr;
+    const int64_t nn = (int64_t)n * n;
+    unsigned k = 0;  // flat item counter (identical in every warp)
+#pragma unroll 1
+    for (unsigned t = 0; t < my_tiles; ++t) {
+        const TileBox b = tile_box(t);
+        if (t + 1 < my_tiles && lane < PP * DD) {
+            // L2 prefetch of this warp's G4 rows of the next tile (one row segment per lane)
+            const TileBox b2 = tile_box(t + 1);
+            const int64_t q = b2.q0 + PP * wq + lane / DD;
+            const int k1 = b2.k1_0 + e0 + lane % DD;
+            const int c0 = b2.j0 + e0 + lane % DD;
+            if (q < P.hi && k1 < n && c0 < n) {
+                const int len = min(32, n - c0);
+                const uintptr_t a0 = reinterpret_cast<uintptr_t>(P.g4 + ((q - P.lo) * n + k1) * (int64_t)n + c0);
+                const uintptr_t a = a0 & ~(uintptr_t)15;
+                const uint32_t bytes = (uint32_t)(a0 - a + len * sizeof(Cx<R>)) & ~15u;
+                if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
+            }
+        }
+        const int c = b.j0 + lane;
+        const bool col_ok = c < n;
+        const int64_t qw = b.q0 + PP * wq;
+        Cx<R>* gb = P.g4 + (qw - P.lo) * nn;
+        uint32_t okmask = 0;
+#pragma unroll
+        for (int p = 0; p < PP; ++p)
+#pragma unroll
+            for (int d = 0; d < DD; ++d)
+                if (col_ok && (qw + p) < P.hi && (b.k1_0 + e0 + d) < n) okmask |= 1u << (p * DD + d);
+        Cx<R> acc[PP][DD];
+#pragma unroll
+        for (int p = 0; p < PP; ++p)
+#pragma unroll
+            for (int d = 0; d < DD; ++d) {
+                if (okmask & (1u << (p * DD + d))) {
+                    acc[p][d] = ld_g4(gb + p * nn + wrap(b.k1_0 + e0 + d, n) * n + wrap(c + e0 + d, n));
+                } else {
+                    acc[p][d].re = R(0);
+                    acc[p][d].im = R(0);
+                }
+            }
+        const int sh_o = (PP * wq + DR - DD - e0) * G::W + (31 - lane) + b.ps;
+        const int dr_o = e0 * G::W + lane + b.pd;
+#pragma unroll 1
+        for (int w = 0; w < nb; ++w, ++k) {
+            const int s = (int)(k % NST);
+            mbar_wait(&full[s], (k / NST) & 1);
+            const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
+            const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
+            const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
+            const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
+            Stg<R> dv[DD];
+#pragma unroll
+            for (int d = 0; d < DD; ++d) dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
+            Stg<R> snext = widen<R>(lds_plain(sh_u + sh_o, sh_d + sh_o));
+            // producer duty: refill the stage released in the previous item with item k - 1 + NST
+            if (producer && k >= 1 && k - 1 + NST < items) {
+                mbar_wait(&empty[(k - 1) % NST], ((k - 1) / NST) & 1);
+                issue(k - 1 + NST);
+            }
+#pragma unroll
+            for (int j = 0; j < PP + DD - 1; ++j) {
+                const Stg<R> S = snext;
+                if (j + 1 < PP + DD - 1)
+                    snext = widen<R>(lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W));
+#pragma unroll
+                for (int d = 0; d < DD; ++d) {
+                    const int p = j + d - (DD - 1);
+                    if (p < 0 || p >= PP) continue;
+                    const Stg<R>& D = dv[d];
+                    if constexpr (FUSED) {
+                        update_fused(acc[p][d], S, D);
+                    } else {
+                        R p1r, p1i, p2r, p2i;
+                        cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);
+                        cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);
+                        acc[p][d].re = add_rn(acc[p][d].re, add_rn(p1r, p2r));
+                        acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+#pragma unroll
+        for (int p = 0; p < PP; ++p)
+#pragma unroll
+            for (int d = 0; d < DD; ++d)
+                if (okmask & (1u << (p * DD + d)))
+                    st_g4(gb + p * nn + wrap(b.k1_0 + e0 + d, n) * n + wrap(c + e0 + d, n), acc[p][d]);
+    }
 }
 
 // Host: the two sheared tensor maps of one staged payload, cached by (pointer, n, dtype).
@@ -523,12 +744,19 @@ static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, in
     return G4_OK;
 }
 
-template <typename R, typename RG, class G, bool FUSED, int MINB>
+template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
 static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     static bool attr_set = false;
+    static int ahead = 0;
     if (!attr_set) {
-        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB>,
+        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+        int dev = 0, sms = 0, per_sm = 0;
+        G4_CUDA(cudaGetDevice(&dev));
+        G4_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        G4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
+                                                              32 * G::CW, G::SMEM));
+        ahead = sms * std::max(per_sm, 1);
         attr_set = true;
     }
     const int n = prm.n;
@@ -540,21 +768,90 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
         tp.hi = prm.hi;
         tp.n = n;
         tp.off = sheared_offset(n, G::ES);
+        tp.ahead = ahead;
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
-            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, G::DD, &mp));
+            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, G::DR, &mp));
             tp.dmap[i] = mp.dmap;
             tp.smap[i] = mp.smap;
         }
         const int64_t planes = prm.hi - prm.lo;
-        tp.nx = (int32_t)((planes + G::PP * G::CW - 1) / (G::PP * G::CW));
-        const uint64_t ctas = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DD - 1) / G::DD);
+        tp.nx = (int32_t)((planes + G::Q - 1) / G::Q);
+        const uint64_t ctas = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
         if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
-        k_accumulate_tma<R, RG, G, FUSED, MINB><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
+        k_accumulate_tma<R, RG, G, FUSED, MINB, EXP><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
         G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
     }
     return G4_OK;
+}
+
+template <typename R, typename RG, class G, bool FUSED, int MINB>
+static g4_status launch_v3(const AccParams<R, RG>& prm, cudaStream_t st) {
+    static bool attr_set = false;
+    static int resident = 0;
+    if (!attr_set) {
+        G4_CUDA(cudaFuncSetAttribute(k_accumulate_pers<R, RG, G, FUSED, MINB>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+        int dev = 0, sms = 0, per_sm = 0;
+        G4_CUDA(cudaGetDevice(&dev));
+        G4_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+        G4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accumulate_pers<R, RG, G, FUSED, MINB>,
+                                                              32 * G::CW, G::SMEM));
+        resident = sms * std::max(per_sm, 1);
+        attr_set = true;
+    }
+    const int n = prm.n;
+    for (int b0 = 0; b0 < prm.nbatch; b0 += TMA_MAXW) {
+        TmaParams<R> tp;
+        std::memset(&tp, 0, sizeof(tp));
+        tp.g4 = prm.g4;
+        tp.lo = prm.lo;
+        tp.hi = prm.hi;
+        tp.n = n;
+        tp.off = sheared_offset(n, G::ES);
+        tp.ahead = resident;
+        tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
+        for (int i = 0; i < tp.nbatch; ++i) {
+            MapPair mp;
+            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, G::DR, &mp));
+            tp.dmap[i] = mp.dmap;
+            tp.smap[i] = mp.smap;
+        }
+        const int64_t planes = prm.hi - prm.lo;
+        tp.nx = (int32_t)((planes + G::Q - 1) / G::Q);
+        const uint64_t tiles = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
+        if (tiles >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: too many tiles");
+        const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)resident);
+        k_accumulate_pers<R, RG, G, FUSED, MINB><<<grid, 32 * G::CW, G::SMEM, st>>>(tp);
+        G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_pers launch"));
+    }
+    return G4_OK;
+}
+
+// v3 geometry (G4RING_V3GEOM): see V2Geom.
+static int v3_geom() {
+    static int g = -1;
+    if (g < 0) {
+        const char* e = getenv("G4RING_V3GEOM");
+        g = e ? atoi(e) : 0;
+    }
+    return g;
+}
+
+template <typename R, typename RG, bool FUSED>
+static g4_status launch_v3_auto(const AccParams<R, RG>& prm, cudaStream_t st) {
+    if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
+        switch (v3_geom()) {
+            case 1: return launch_v3<R, RG, V2Geom<RG, 4, 4, 3, 4, 2>, FUSED, 2>(prm, st);
+            case 2: return launch_v3<R, RG, V2Geom<RG, 4, 4, 2, 4, 2>, FUSED, 2>(prm, st);
+            case 3: return launch_v3<R, RG, V2Geom<RG, 4, 4, 3, 4, 1>, FUSED, 3>(prm, st);
+            case 4: return launch_v3<R, RG, V2Geom<RG, 8, 2, 3, 4, 2>, FUSED, 2>(prm, st);
+            case 5: return launch_v3<R, RG, V2Geom<RG, 4, 4, 4, 4, 4>, FUSED, 1>(prm, st);
+            default: return launch_v3<R, RG, V2Geom<RG, 4, 4, 2, 4, 1>, FUSED, 4>(prm, st);
+        }
+    }
+    return launch_v3<R, RG, V2Geom<RG, 4, 4, 2, 4, 1>, FUSED, 4>(prm, st);
 }
 
 // v2 geometry selection (G4RING_V2GEOM overrides for measurements):
@@ -578,7 +875,33 @@ static g4_status launch_v2_auto(const AccParams<R, RG>& prm, cudaStream_t st) {
         case 4: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 2>, FUSED, 6>(prm, st);
         case 5: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 3>, FUSED, 5>(prm, st);
         case 6: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 2>, FUSED, 5>(prm, st);
-        default: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
+        case 7: case 8: case 9: case 10: case 11: case 12: case 13: case 14: case 15:
+            if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
+                switch (v2_geom()) {  // CTA tiles with CWR > 1 warp rows along the diagonal
+                    case 7: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 2>, FUSED, 2>(prm, st);
+                    case 8: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 4>, FUSED, 1>(prm, st);
+                    case 9: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 4, 4>, FUSED, 1>(prm, st);
+                    case 10: return launch_v2<R, RG, V2Geom<RG, 4, 2, 2, 4, 4>, FUSED, 2>(prm, st);
+                    case 11: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 4, 2>, FUSED, 2>(prm, st);
+                    case 13: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4>(prm, st);
+                    case 14: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 2, 2>, FUSED, 3>(prm, st);
+                    case 15: return launch_v2<R, RG, V2Geom<RG, 16, 1, 2, 1, 4>, FUSED, 4>(prm, st);
+                    default: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2>, FUSED, 2>(prm, st);
+                }
+            }
+            return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM 7-12 are complex128 only");
+        default:
+            if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
+                switch (exp_flags()) {  // measurement variants (complex128 only)
+                    case 0: break;
+                    case 3: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 3>(prm, st);
+                    case 4: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 4>(prm, st);
+                    case 7: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 7>(prm, st);
+                    case 8: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 8>(prm, st);
+                    default: return fail(G4_ERR_CONTRACT, "G4RING_EXP: unknown variant");
+                }
+            }
+            return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
     }
 }
 
@@ -587,6 +910,7 @@ template <typename R, typename RG, bool FUSED>
 static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     const int variant = kernel_variant();
+    if (variant == 3 && prm.n >= 64) return launch_v3_auto<R, RG, FUSED>(prm, st);
     if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2_auto<R, RG, FUSED>(prm, st);
     if (variant == 2 && prm.n >= 64) return launch_v2_auto<R, RG, FUSED>(prm, st);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
@@ -649,7 +973,7 @@ g4_status g4_accumulate_staged(void* g4p, int64_t lo, int64_t hi, int32_t n, con
 }
 
 g4_status g4_set_kernel_variant(int32_t variant) {
-    if (variant < 0 || variant > 2)
+    if (variant < 0 || variant > 3)
         return g4::fail(G4_ERR_CONTRACT, "kernel variant must be 0 (auto), 1 (v1) or 2 (v2)");
     g4::g_variant = variant;
     return G4_OK;
