@@ -116,10 +116,12 @@ g4_status g4_accumulate_staged(void* g4, int64_t lo, int64_t hi, int32_t n,
                                const void* const* staged, int32_t nbatch, int32_t dtype,
                                int32_t channel, void* stream);
 
-/* Select the K1 implementation (process-wide): 0 = v1 (register-blocked,
- * L1-shared direct loads; the default), 1 = v2 (TMA-bulk staged through a
- * shared-memory ring, warp-specialised; used for N >= 64).  For A/B
- * measurement and parity tests of both paths (env G4RING_KERNEL). */
+/* Select the K1 implementation (process-wide): 0 = automatic (v2 for N >= 64
+ * and >= 4 planes, with a 16-plane CTA tile for >= 16 planes and an 8-plane
+ * tile below; v1 otherwise), 1 = v1 everywhere (register-blocked, direct
+ * global loads), 2 = v2 wherever N >= 64 (TMA tensor boxes into a
+ * shared-memory ring).  For A/B measurement and parity tests of both paths
+ * (env G4RING_KERNEL; G4RING_V2GEOM forces a v2 geometry). */
 g4_status g4_set_kernel_variant(int32_t variant);
 
 /* Floating-point evaluation of the update (process-wide):

@@ -515,168 +515,6 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
             }
 }
 
-// ---------------------------------------------------------------------------
-// v3 -- persistent CTAs.  Same tile, operand staging and arithmetic as v2, but
-// each CTA walks tiles lin = blockIdx.x + t * gridDim.x (the L2-aware order)
-// and the shared-memory ring runs continuously over the flat item sequence
-// (tile, walker): the producer keeps NST - 1 payload boxes in flight across
-// tile boundaries, so a tile's first walker is already resident when its G4
-// block has been read.  The G4 rows of the CTA's next tile are prefetched into
-// L2 while the current tile computes.
-template <typename R, typename RG, class G, bool FUSED, int MINB>
-__global__ void __launch_bounds__(32 * G::CW, MINB)
-k_accumulate_pers(const __grid_constant__ TmaParams<R> P) {
-    constexpr int PP = G::PP, DD = G::DD, NST = G::NST, DR = G::DR, Q = G::Q;
-    constexpr int EW = G::ES / 8;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NST * G::STAGE_BYTES);
-    uint64_t* empty = full + NST;
-
-    const int n = P.n;
-    const int nb = P.nbatch;
-    const int ny = (n + 31) / 32, nz = (n + DR - 1) / DR;
-    const unsigned ntiles = (unsigned)P.nx * ny * nz;
-    if (blockIdx.x >= ntiles) return;
-    const unsigned my_tiles = (ntiles - blockIdx.x + gridDim.x - 1) / gridDim.x;
-    const unsigned items = my_tiles * (unsigned)nb;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const bool producer = threadIdx.x == 0;
-
-    // Tile geometry (see k_accumulate_tma): sheared box starts of the direct
-    // tile and the shifted band, with the 16-B parity shift for complex64.
-    struct TileBox {
-        int64_t q0;
-        int j0, k1_0, xd, xs, R0, pd, ps;
-    };
-    auto tile_box = [&](unsigned t) {
-        const TileCoord tc = tile_coord(blockIdx.x + t * gridDim.x, P.nx, ny, nz);
-        TileBox b;
-        b.q0 = P.lo + (int64_t)tc.x * Q;
-        b.j0 = tc.y * 32;
-        b.k1_0 = tc.z * DR;
-        b.R0 = wrap((int)(b.q0 - b.k1_0) - (DR - 1), n);
-        const int C0 = wrap((int)(b.q0 - b.j0) - 31 - (DR - 1), n);
-        b.xd = b.j0 - b.k1_0 + P.off;
-        b.xs = C0 - b.R0 + P.off;
-        b.pd = (G::ES == 8) ? (b.xd & 1) : 0;
-        b.ps = (G::ES == 8) ? (b.xs & 1) : 0;
-        return b;
-    };
-    auto issue = [&](unsigned k) {  // producer lane: item k = (tile k / nb, walker k % nb)
-        const int s = (int)(k % NST);
-        const unsigned t = k / (unsigned)nb;
-        const int w = (int)(k - t * (unsigned)nb);
-        const TileBox b = tile_box(t);
-        mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
-        unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
-        tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (b.xd - b.pd), b.k1_0, 0, &full[s]);
-        tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (b.xs - b.ps), b.R0, 0, &full[s]);
-    };
-    if (producer) {
-        for (int s = 0; s < NST; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], G::CW);
-        }
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (unsigned k = 0; k < (unsigned)NST && k < items; ++k) issue(k);
-    }
-    __syncthreads();
-
-    const int wq = warp % G::CWQ, wr = warp / G::CWQ;
-    const int e0 = DD * wr;
-    const int64_t nn = (int64_t)n * n;
-    unsigned k = 0;  // flat item counter (identical in every warp)
-#pragma unroll 1
-    for (unsigned t = 0; t < my_tiles; ++t) {
-        const TileBox b = tile_box(t);
-        if (t + 1 < my_tiles && lane < PP * DD) {
-            // L2 prefetch of this warp's G4 rows of the next tile (one row segment per lane)
-            const TileBox b2 = tile_box(t + 1);
-            const int64_t q = b2.q0 + PP * wq + lane / DD;
-            const int k1 = b2.k1_0 + e0 + lane % DD;
-            const int c0 = b2.j0 + e0 + lane % DD;
-            if (q < P.hi && k1 < n && c0 < n) {
-                const int len = min(32, n - c0);
-                const uintptr_t a0 = reinterpret_cast<uintptr_t>(P.g4 + ((q - P.lo) * n + k1) * (int64_t)n + c0);
-                const uintptr_t a = a0 & ~(uintptr_t)15;
-                const uint32_t bytes = (uint32_t)(a0 - a + len * sizeof(Cx<R>)) & ~15u;
-                if (bytes) asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
-            }
-        }
-        const int c = b.j0 + lane;
-        const bool col_ok = c < n;
-        const int64_t qw = b.q0 + PP * wq;
-        Cx<R>* gb = P.g4 + (qw - P.lo) * nn;
-        uint32_t okmask = 0;
-#pragma unroll
-        for (int p = 0; p < PP; ++p)
-#pragma unroll
-            for (int d = 0; d < DD; ++d)
-                if (col_ok && (qw + p) < P.hi && (b.k1_0 + e0 + d) < n) okmask |= 1u << (p * DD + d);
-        Cx<R> acc[PP][DD];
-#pragma unroll
-        for (int p = 0; p < PP; ++p)
-#pragma unroll
-            for (int d = 0; d < DD; ++d) {
-                if (okmask & (1u << (p * DD + d))) {
-                    acc[p][d] = ld_g4(gb + p * nn + wrap(b.k1_0 + e0 + d, n) * n + wrap(c + e0 + d, n));
-                } else {
-                    acc[p][d].re = R(0);
-                    acc[p][d].im = R(0);
-                }
-            }
-        const int sh_o = (PP * wq + DR - DD - e0) * G::W + (31 - lane) + b.ps;
-        const int dr_o = e0 * G::W + lane + b.pd;
-#pragma unroll 1
-        for (int w = 0; w < nb; ++w, ++k) {
-            const int s = (int)(k % NST);
-            mbar_wait(&full[s], (k / NST) & 1);
-            const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
-            const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
-            const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
-            const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
-            Stg<R> dv[DD];
-#pragma unroll
-            for (int d = 0; d < DD; ++d) dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
-            Stg<R> snext = widen<R>(lds_plain(sh_u + sh_o, sh_d + sh_o));
-            // producer duty: refill the stage released in the previous item with item k - 1 + NST
-            if (producer && k >= 1 && k - 1 + NST < items) {
-                mbar_wait(&empty[(k - 1) % NST], ((k - 1) / NST) & 1);
-                issue(k - 1 + NST);
-            }
-#pragma unroll
-            for (int j = 0; j < PP + DD - 1; ++j) {
-                const Stg<R> S = snext;
-                if (j + 1 < PP + DD - 1)
-                    snext = widen<R>(lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W));
-#pragma unroll
-                for (int d = 0; d < DD; ++d) {
-                    const int p = j + d - (DD - 1);
-                    if (p < 0 || p >= PP) continue;
-                    const Stg<R>& D = dv[d];
-                    if constexpr (FUSED) {
-                        update_fused(acc[p][d], S, D);
-                    } else {
-                        R p1r, p1i, p2r, p2i;
-                        cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);
-                        cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);
-                        acc[p][d].re = add_rn(acc[p][d].re, add_rn(p1r, p2r));
-                        acc[p][d].im = add_rn(acc[p][d].im, add_rn(p1i, p2i));
-                    }
-                }
-            }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
-        }
-#pragma unroll
-        for (int p = 0; p < PP; ++p)
-#pragma unroll
-            for (int d = 0; d < DD; ++d)
-                if (okmask & (1u << (p * DD + d)))
-                    st_g4(gb + p * nn + wrap(b.k1_0 + e0 + d, n) * n + wrap(c + e0 + d, n), acc[p][d]);
-    }
-}
-
 // Host: the two sheared tensor maps of one staged payload, cached by (pointer, n, dtype).
 using PFN_encodeTiled = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
                                      const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
@@ -691,16 +529,21 @@ struct MapPair {
 // is non-negative, and the map's base (stg - off * es) stays 16-B aligned.
 static int sheared_offset(int n, int es) { return (es == 8 && (n & 1)) ? n + 1 : n; }
 
-static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, int dd, MapPair* out) {
+static PFN_encodeTiled tensor_map_encoder() {
     static PFN_encodeTiled encode = nullptr;
     if (!encode) {
         cudaDriverEntryPointQueryResult q{};
         void* fn = nullptr;
         cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
-        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn)
-            return fail(G4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return nullptr;
         encode = reinterpret_cast<PFN_encodeTiled>(fn);
     }
+    return encode;
+}
+
+static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, int dd, MapPair* out) {
+    PFN_encodeTiled encode = tensor_map_encoder();
+    if (!encode) return fail(G4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t ld = (cuuint64_t)staged_ld(n, es), rows = (cuuint64_t)staged_rows(n, es);
     const cuuint64_t plane_b = (cuuint64_t)staged_plane(n, es) * es;
     const cuuint32_t ew = es / 8;  // 64-bit elements per complex entry
@@ -786,111 +629,20 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     return G4_OK;
 }
 
-template <typename R, typename RG, class G, bool FUSED, int MINB>
-static g4_status launch_v3(const AccParams<R, RG>& prm, cudaStream_t st) {
-    static bool attr_set = false;
-    static int resident = 0;
-    if (!attr_set) {
-        G4_CUDA(cudaFuncSetAttribute(k_accumulate_pers<R, RG, G, FUSED, MINB>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-        int dev = 0, sms = 0, per_sm = 0;
-        G4_CUDA(cudaGetDevice(&dev));
-        G4_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        G4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accumulate_pers<R, RG, G, FUSED, MINB>,
-                                                              32 * G::CW, G::SMEM));
-        resident = sms * std::max(per_sm, 1);
-        attr_set = true;
-    }
-    const int n = prm.n;
-    for (int b0 = 0; b0 < prm.nbatch; b0 += TMA_MAXW) {
-        TmaParams<R> tp;
-        std::memset(&tp, 0, sizeof(tp));
-        tp.g4 = prm.g4;
-        tp.lo = prm.lo;
-        tp.hi = prm.hi;
-        tp.n = n;
-        tp.off = sheared_offset(n, G::ES);
-        tp.ahead = resident;
-        tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
-        for (int i = 0; i < tp.nbatch; ++i) {
-            MapPair mp;
-            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, G::DR, &mp));
-            tp.dmap[i] = mp.dmap;
-            tp.smap[i] = mp.smap;
-        }
-        const int64_t planes = prm.hi - prm.lo;
-        tp.nx = (int32_t)((planes + G::Q - 1) / G::Q);
-        const uint64_t tiles = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
-        if (tiles >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: too many tiles");
-        const unsigned grid = (unsigned)std::min<uint64_t>(tiles, (uint64_t)resident);
-        k_accumulate_pers<R, RG, G, FUSED, MINB><<<grid, 32 * G::CW, G::SMEM, st>>>(tp);
-        G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_pers launch"));
-    }
-    return G4_OK;
-}
-
-// v3 geometry (G4RING_V3GEOM): see V2Geom.
-static int v3_geom() {
-    static int g = -1;
-    if (g < 0) {
-        const char* e = getenv("G4RING_V3GEOM");
-        g = e ? atoi(e) : 0;
-    }
-    return g;
-}
-
+// v2 geometries: PP x DD thread block, CWQ x CWR warps (CTA tile Q x DR), NST
+// stages, CTAs per SM.  Sweep results: profiles/r01_summary.md.
+//   id  PPxDD  CWQxCWR  QxDR   NST CTA/SM       id  PPxDD  CWQxCWR  QxDR   NST CTA/SM
+//    0  4x4    4x1      16x4    3   3            12  8x4    2x2      16x8    3   2
+//    3  4x4    4x1      16x4    2   4            13  8x2    2x2      16x4    2   4   (default, P >= 16)
+//    7  4x4    4x2      16x8    2   2            16  4x4    4x1      16x4    4   2
+//    8  4x4    4x4      16x16   2   1            17  8x2    2x2      16x4    4   2
+//   11  4x4    4x2      16x8    3   2            19  8x2    1x4       8x8    2   4   (default, P <= 8)
+//                                                20  4x4    2x2       8x8    2   4
 template <typename R, typename RG, bool FUSED>
-static g4_status launch_v3_auto(const AccParams<R, RG>& prm, cudaStream_t st) {
-    if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
-        switch (v3_geom()) {
-            case 1: return launch_v3<R, RG, V2Geom<RG, 4, 4, 3, 4, 2>, FUSED, 2>(prm, st);
-            case 2: return launch_v3<R, RG, V2Geom<RG, 4, 4, 2, 4, 2>, FUSED, 2>(prm, st);
-            case 3: return launch_v3<R, RG, V2Geom<RG, 4, 4, 3, 4, 1>, FUSED, 3>(prm, st);
-            case 4: return launch_v3<R, RG, V2Geom<RG, 8, 2, 3, 4, 2>, FUSED, 2>(prm, st);
-            case 5: return launch_v3<R, RG, V2Geom<RG, 4, 4, 4, 4, 4>, FUSED, 1>(prm, st);
-            default: return launch_v3<R, RG, V2Geom<RG, 4, 4, 2, 4, 1>, FUSED, 4>(prm, st);
-        }
-    }
-    return launch_v3<R, RG, V2Geom<RG, 4, 4, 2, 4, 1>, FUSED, 4>(prm, st);
-}
-
-// v2 geometry selection (G4RING_V2GEOM overrides for measurements):
-//   0: PP=4, CW=4, 3 stages, 3 CTAs/SM      1: PP=8, CW=2, 3 stages
-//   2: PP=8, CW=4, 2 stages                 3: PP=4, CW=4, 2 stages, 4 CTAs/SM -- the default
-static int v2_geom() {
-    static int g = -1;
-    if (g < 0) {
-        const char* e = getenv("G4RING_V2GEOM");
-        g = e ? atoi(e) : 3;
-    }
-    return g;
-}
-
-template <typename R, typename RG, bool FUSED>
-static g4_status launch_v2_auto(const AccParams<R, RG>& prm, cudaStream_t st) {
-    switch (v2_geom()) {
+static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
+    switch (g) {
         case 0: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3>, FUSED, 3>(prm, st);
-        case 1: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3>, FUSED, 3>(prm, st);
-        case 2: return launch_v2<R, RG, V2Geom<RG, 8, 4, 2>, FUSED, 2>(prm, st);
-        case 4: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 2>, FUSED, 6>(prm, st);
-        case 5: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 3>, FUSED, 5>(prm, st);
-        case 6: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 2>, FUSED, 5>(prm, st);
-        case 7: case 8: case 9: case 10: case 11: case 12: case 13: case 14: case 15:
-            if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
-                switch (v2_geom()) {  // CTA tiles with CWR > 1 warp rows along the diagonal
-                    case 7: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 2>, FUSED, 2>(prm, st);
-                    case 8: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 4>, FUSED, 1>(prm, st);
-                    case 9: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 4, 4>, FUSED, 1>(prm, st);
-                    case 10: return launch_v2<R, RG, V2Geom<RG, 4, 2, 2, 4, 4>, FUSED, 2>(prm, st);
-                    case 11: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 4, 2>, FUSED, 2>(prm, st);
-                    case 13: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4>(prm, st);
-                    case 14: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 2, 2>, FUSED, 3>(prm, st);
-                    case 15: return launch_v2<R, RG, V2Geom<RG, 16, 1, 2, 1, 4>, FUSED, 4>(prm, st);
-                    default: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2>, FUSED, 2>(prm, st);
-                }
-            }
-            return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM 7-12 are complex128 only");
-        default:
+        case 3:
             if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
                 switch (exp_flags()) {  // measurement variants (complex128 only)
                     case 0: break;
@@ -902,7 +654,29 @@ static g4_status launch_v2_auto(const AccParams<R, RG>& prm, cudaStream_t st) {
                 }
             }
             return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
+        case 7: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 2>, FUSED, 2>(prm, st);
+        case 8: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 4>, FUSED, 1>(prm, st);
+        case 11: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 4, 2>, FUSED, 2>(prm, st);
+        case 12: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2>, FUSED, 2>(prm, st);
+        case 13: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4>(prm, st);
+        case 16: return launch_v2<R, RG, V2Geom<RG, 4, 4, 4>, FUSED, 2>(prm, st);
+        case 17: return launch_v2<R, RG, V2Geom<RG, 8, 2, 4, 2, 2>, FUSED, 2>(prm, st);
+        case 19: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4>(prm, st);
+        case 20: return launch_v2<R, RG, V2Geom<RG, 4, 2, 2, 4, 2>, FUSED, 4>(prm, st);
+        default: return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
     }
+}
+
+// Automatic choice: a 16-plane CTA tile when the slice has >= 16 planes, an
+// 8-plane tile for the 8-plane slices of an 8-GPU ring.  G4RING_V2GEOM overrides.
+static int v2_geom(int64_t planes) {
+    static int forced = -2;
+    if (forced == -2) {
+        const char* e = getenv("G4RING_V2GEOM");
+        forced = e ? atoi(e) : -1;
+    }
+    if (forced >= 0) return forced;
+    return planes >= 16 ? 13 : 19;
 }
 
 // ---------------------------------------------------------------------------
@@ -910,9 +684,8 @@ template <typename R, typename RG, bool FUSED>
 static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     const int variant = kernel_variant();
-    if (variant == 3 && prm.n >= 64) return launch_v3_auto<R, RG, FUSED>(prm, st);
-    if (variant != 1 && prm.n >= 64 && planes > 8) return launch_v2_auto<R, RG, FUSED>(prm, st);
-    if (variant == 2 && prm.n >= 64) return launch_v2_auto<R, RG, FUSED>(prm, st);
+    if (prm.n >= 64 && (variant == 2 || (variant == 0 && planes >= 4)))
+        return launch_v2_geom<R, RG, FUSED>(v2_geom(planes), prm, st);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
@@ -973,7 +746,7 @@ g4_status g4_accumulate_staged(void* g4p, int64_t lo, int64_t hi, int32_t n, con
 }
 
 g4_status g4_set_kernel_variant(int32_t variant) {
-    if (variant < 0 || variant > 3)
+    if (variant < 0 || variant > 2)
         return g4::fail(G4_ERR_CONTRACT, "kernel variant must be 0 (auto), 1 (v1) or 2 (v2)");
     g4::g_variant = variant;
     return G4_OK;
