@@ -295,6 +295,7 @@ def run_gpu(args):
                      "frac": achieved / peak, "traffic": None,
                      "peak_source": peak_kind, "kernel": "k_accumulate",
                      "bytes_per_launch": alg_bytes},
+        "onchip": onchip_bounds(lib, n, planes, args.dtype, args.arith, B, upd_step / (statistics.mean(k_ms) * 1e-3)),
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": args.steps,
@@ -311,6 +312,50 @@ def run_gpu(args):
                       f"numpy port of accumulate_g4 in {used} processes on disjoint K3 ranges; "
                       f"host {cpu_model()}"}
     print(json.dumps(line), flush=True)
+
+
+# On-chip ceilings of K1 (calibrated with tools/microbench.cu, profiles/r01_microbench.txt):
+# conflict-free LDS.128 126 B/clk/SM, DFMA 17.0 T instr/s, FFMA 35.7 T instr/s.
+SMEM_B_PER_CLK_SM = 126.0
+FP64_INSTR_PEAK = 17.0e12
+FP32_INSTR_PEAK = 35.7e12
+
+
+def onchip_bounds(lib, n, planes, dtype, arith, B, upd_per_s):
+    """Per-update traffic through each SM's shared-memory/L1 data path and FP
+    instruction count of the K1 launch actually used (g4_k1_config), with the
+    fraction of each measured ceiling the kernel reaches.  At B >= 4 these,
+    not HBM, bound K1."""
+    import ctypes
+    import torch
+    code = {"c128": 0, "c64": 1, "mixed": 2}[dtype]
+    cfg = (ctypes.c_int32 * 8)()
+    lib.g4_k1_config(n, planes, code, cfg)
+    variant, pp, dd, q, dr, nst, ctas, warps = list(cfg)
+    eb = 8 if dtype == "c64" else 16          # G4 entry
+    peb = 16 if dtype == "c128" else 8        # payload entry
+    lds = 2 * peb * (pp + 2 * dd - 1) / (pp * dd)            # operand loads per update
+    width = 32 if peb == 16 else 34
+    fill = 2 * peb * width * (dr + q + dr - 1) / (q * dr * 32) if variant == 2 else 0.0  # TMA writes
+    g4 = 2 * eb / B                                          # G4 block in and out through L1
+    path = lds + fill + g4
+    props = torch.cuda.get_device_properties(torch.cuda.current_device())
+    clock_hz = 1965e6
+    smem_peak = SMEM_B_PER_CLK_SM * props.multi_processor_count * clock_hz
+    instr = (8 if arith == "fused" else 12)
+    fpeak = FP32_INSTR_PEAK if dtype == "c64" else FP64_INSTR_PEAK
+    return {
+        "k1": {"variant": variant, "thread_block": [pp, dd], "cta_tile": [q, dr], "stages": nst,
+               "ctas_per_sm": ctas, "warps_per_cta": warps},
+        "smem_path_bytes_per_update": {"operand_lds": lds, "tma_fill": fill, "g4_via_l1": g4, "total": path},
+        "smem_path_achieved_TBps": path * upd_per_s / 1e12,
+        "smem_path_peak_TBps": smem_peak / 1e12,
+        "smem_frac": path * upd_per_s / smem_peak,
+        "fp_instr_per_update": instr, "fp_pipe": "fp32" if dtype == "c64" else "fp64",
+        "fp_achieved_Tinstr": instr * upd_per_s / 1e12, "fp_peak_Tinstr": fpeak / 1e12,
+        "fp_frac": instr * upd_per_s / fpeak,
+        "peak_source": "tools/microbench.cu (profiles/r01_microbench.txt) at 1965 MHz",
+    }
 
 
 def max_g4_capacity(dev, n=4608, walkers=8, margin=6e9):

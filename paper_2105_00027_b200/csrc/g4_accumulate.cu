@@ -667,6 +667,31 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
     }
 }
 
+// Host-side description of a geometry id (same table as launch_v2_geom).
+struct GeomInfo {
+    int pp, dd, q, dr, nst, ctas, warps;
+};
+template <class G>
+static GeomInfo info_of(int ctas) {
+    return {G::PP, G::DD, G::Q, G::DR, G::NST, ctas, G::CW};
+}
+static bool geom_info(int g, GeomInfo* out) {
+    switch (g) {
+        case 0: *out = info_of<V2Geom<double, 4, 4, 3>>(3); return true;
+        case 3: *out = info_of<V2Geom<double, 4, 4, 2>>(4); return true;
+        case 7: *out = info_of<V2Geom<double, 4, 4, 2, 4, 2>>(2); return true;
+        case 8: *out = info_of<V2Geom<double, 4, 4, 2, 4, 4>>(1); return true;
+        case 11: *out = info_of<V2Geom<double, 4, 4, 3, 4, 2>>(2); return true;
+        case 12: *out = info_of<V2Geom<double, 8, 2, 3, 4, 2>>(2); return true;
+        case 13: *out = info_of<V2Geom<double, 8, 2, 2, 2, 2>>(4); return true;
+        case 16: *out = info_of<V2Geom<double, 4, 4, 4>>(2); return true;
+        case 17: *out = info_of<V2Geom<double, 8, 2, 4, 2, 2>>(2); return true;
+        case 19: *out = info_of<V2Geom<double, 8, 1, 2, 2, 4>>(4); return true;
+        case 20: *out = info_of<V2Geom<double, 4, 2, 2, 4, 2>>(4); return true;
+        default: return false;
+    }
+}
+
 // Automatic choice: a 16-plane CTA tile when the slice has >= 16 planes, an
 // 8-plane tile for the 8-plane slices of an 8-GPU ring.  G4RING_V2GEOM overrides.
 static int v2_geom(int64_t planes) {
@@ -680,12 +705,15 @@ static int v2_geom(int64_t planes) {
 }
 
 // ---------------------------------------------------------------------------
+static bool use_v2(int n, int64_t planes) {
+    const int variant = kernel_variant();
+    return n >= 64 && (variant == 2 || (variant == 0 && planes >= 4));
+}
+
 template <typename R, typename RG, bool FUSED>
 static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
-    const int variant = kernel_variant();
-    if (prm.n >= 64 && (variant == 2 || (variant == 0 && planes >= 4)))
-        return launch_v2_geom<R, RG, FUSED>(v2_geom(planes), prm, st);
+    if (use_v2(prm.n, planes)) return launch_v2_geom<R, RG, FUSED>(v2_geom(planes), prm, st);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
@@ -749,6 +777,25 @@ g4_status g4_set_kernel_variant(int32_t variant) {
     if (variant < 0 || variant > 2)
         return g4::fail(G4_ERR_CONTRACT, "kernel variant must be 0 (auto), 1 (v1) or 2 (v2)");
     g4::g_variant = variant;
+    return G4_OK;
+}
+
+g4_status g4_k1_config(int32_t n, int64_t planes, int32_t dtype, int32_t* out) {
+    using namespace g4;
+    if (!out) return fail(G4_ERR_CONTRACT, "k1_config: null output");
+    if (n < 1 || planes < 1) return fail(G4_ERR_CONTRACT, "k1_config: n and planes must be >= 1");
+    if (dtype != G4_C128 && dtype != G4_C64 && dtype != G4_C128_G64) return fail(G4_ERR_CONTRACT, "unknown dtype");
+    if (use_v2(n, planes)) {
+        GeomInfo gi;
+        if (!geom_info(v2_geom(planes), &gi)) return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
+        const int32_t v[8] = {2, gi.pp, gi.dd, gi.q, gi.dr, gi.nst, gi.ctas, gi.warps};
+        std::memcpy(out, v, sizeof(v));
+    } else {
+        const int warps = planes <= 4 ? 1 : planes <= 8 ? 2 : 4;
+        const int ctas = planes <= 4 ? 12 : planes <= 8 ? 6 : 3;
+        const int32_t v[8] = {1, 4, 4, 4 * warps, 4, 0, ctas, warps};
+        std::memcpy(out, v, sizeof(v));
+    }
     return G4_OK;
 }
 
