@@ -524,17 +524,19 @@ def run_ring(args):
         world.barrier()
         torch.cuda.synchronize(dev)
         t0.record(eng.compute)
+        h0 = time.perf_counter()
         for i in range(args.steps):
             eng.enqueue_round(regenerate=False)
+        host_ms = (time.perf_counter() - h0) * 1e3 / args.steps
         t1.record(eng.compute)
         eng.wait_idle(300.0)
         torch.cuda.synchronize(dev)
         world.barrier()
     ms_local = t0.elapsed_time(t1) / args.steps
-    k_ms = [a.elapsed_time(b) for a, b in eng.kernel_events]
-    stats = world.allgather({"ms": ms_local, "k_ms": statistics.mean(k_ms), "clk": clk.summary(),
-                             "lo": eng.lo, "hi": eng.hi})
+    stats = world.allgather({"ms": ms_local, "k_ms": eng.k1_mean_ms(), "clk": clk.summary(),
+                             "lo": eng.lo, "hi": eng.hi, "host_ms": host_ms})
     e2e = run_ring_e2e(args, eng, world, dev)
+    eng_native = eng.native
     eng.close()
     if rank != 0:
         return
@@ -566,9 +568,23 @@ def run_ring(args):
                    "peak_source": "B200_PROFILING.md measured peer copy"},
         "clocks": stats[0]["clk"],
         "e2e": e2e,
+        "host": {"enqueue_ms_per_step": max(x["host_ms"] for x in stats),
+                 "native_rounds": eng_native,
+                 "note": "host time to issue one round (one C call with the native round program)"},
+        "model": ring_model_line(n, planes, n_ranks, B, args.dtype),
         "gpu_launches": args.steps * n_ranks,  # K1 launches per rank per step = S (own + S-1 received)
     }
     print(json.dumps(line), flush=True)
+
+
+def ring_model_line(n, planes, gpus, batch, dtype):
+    """The NVLink-5 ring model's prediction for this run (paper_2105_00027_b200.model)."""
+    from paper_2105_00027_b200 import model as M
+    r = M.ring_round_time(gpus, batch, n, planes, dtype)
+    return {"round_ms": r["round_s"] * 1e3, "k1_ms": r["k1_s"] * 1e3, "step_transfer_ms": r["transfer_s"] * 1e3,
+            "ring_hidden": r["hidden"], "updates_per_s": r["updates_per_s"],
+            "hide_from_planes_per_gpu": M.hide_planes(n, batch, dtype),
+            "link": "NVSwitch B200 (770 GB/s per direction, 8 us per step; model.NVSWITCH_B200)"}
 
 
 def run_ring_e2e(args, eng, world, dev):

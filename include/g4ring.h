@@ -186,6 +186,33 @@ g4_status g4_flag_host_wait(const void* flag, uint64_t value, int64_t timeout_ms
 g4_status g4_reduce_sum(void* dst, const void* const* src, int32_t nsrc, int64_t count,
                         int32_t dtype, void* stream);
 
+/* ---- native round program (replaces the per-op host loop of the reference's
+ * run_measurement ring phase, engine.py:119-161, for the steady state).  A
+ * round's op list is compiled once; g4_round_program_run(m) then issues every
+ * K3/K1 launch, peer copy, flag write/wait and stream-event dependency of
+ * round m in one host call.  Ops are G4_OP_WORDS int64 words each:
+ *   {G4_OP_ACC,   stream, ptr_off, count}        K1 on ptrs[ptr_off .. +count)
+ *   {G4_OP_WAIT,  stream, flag, base, slope}     wait flag >= base + slope*m
+ *   {G4_OP_WRITE, stream, flag, base, slope}     write base + slope*m
+ *   {G4_OP_COPY,  stream, dst, src, nbytes}      peer copy
+ *   {G4_OP_RECORD / G4_OP_WAIT_EVENT, stream, event}
+ *   {G4_OP_GEN,   stream, ptr_off, count, meta_off}  K3 into ptrs with
+ *       meta[meta_off ..] = world_rank[count], lane[count], meas_base[count];
+ *       meas = meas_base + m * batch (skipped when regenerate == 0).
+ * streams/ptrs are borrowed for the program's lifetime; events are owned. */
+#define G4_OP_WORDS 8
+enum { G4_OP_ACC = 1, G4_OP_WAIT = 2, G4_OP_WRITE = 3, G4_OP_COPY = 4, G4_OP_RECORD = 5,
+       G4_OP_WAIT_EVENT = 6, G4_OP_GEN = 7 };
+g4_status g4_round_program_create(const int64_t* ops, int32_t nops, void* const* ptrs, int32_t nptrs,
+                                  const int64_t* meta, int32_t nmeta, void* const* streams, int32_t nstreams,
+                                  int32_t nevents, void* g4, int64_t lo, int64_t hi, int32_t n, int32_t dtype,
+                                  int32_t pdtype, uint64_t seed, int32_t mode, int64_t batch, int32_t timing,
+                                  void** prog_out);
+g4_status g4_round_program_run(void* prog, int64_t m, int32_t regenerate);
+/* Mean duration of the K1 launches of the last completed round (timing programs). */
+g4_status g4_round_program_k1_ms(void* prog, double* mean_ms, int32_t* count);
+g4_status g4_round_program_destroy(void* prog);
+
 #ifdef __cplusplus
 }
 #endif

@@ -23,6 +23,8 @@ G4_ARITH_EXACT, G4_ARITH_FUSED = 0, 1
 G4_MAX_BATCH = 64
 G4_IPC_HANDLE_BYTES = 64
 G4_HALO_ROWS, G4_HALO_COLS = 40, 72
+G4_OP_WORDS = 8
+G4_OP_ACC, G4_OP_WAIT, G4_OP_WRITE, G4_OP_COPY, G4_OP_RECORD, G4_OP_WAIT_EVENT, G4_OP_GEN = range(1, 8)
 ABI_VERSION = 1
 
 # (name, restype, argtypes) for every symbol include/g4ring.h declares.
@@ -52,6 +54,11 @@ SIGNATURES = {
     "g4_flag_wait": (_i32, [_vp, _u64, _vp]),
     "g4_flag_host_wait": (_i32, [_vp, _u64, _i64]),
     "g4_reduce_sum": (_i32, [_vp, _vpp, _i32, _i64, _i32, _vp]),
+    "g4_round_program_create": (_i32, [_i64p, _i32, _vpp, _i32, _i64p, _i32, _vpp, _i32, _i32, _vp, _i64, _i64,
+                                       _i32, _i32, _i32, _u64, _i32, _i64, _i32, _vpp]),
+    "g4_round_program_run": (_i32, [_vp, _i64, _i32]),
+    "g4_round_program_k1_ms": (_i32, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]),
+    "g4_round_program_destroy": (_i32, [_vp]),
 }
 
 _lock = threading.Lock()

@@ -12,6 +12,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <vector>
 
 #include <cuda.h>
 
@@ -220,6 +221,171 @@ g4_status g4_reduce_sum(void* dst, const void* const* src, int32_t nsrc, int64_t
         return fail(G4_ERR_CONTRACT, "reduce_sum: unknown dtype");
     }
     G4_CUDA(cudaGetLastError());
+    return G4_OK;
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Native round program: the per-op loop of engine.RingEngine.enqueue_round
+// compiled once into a flat op list and replayed per round m with its flag
+// values affine in m (value = base + slope * m).  One host call per round
+// issues every K3/K1 launch, peer copy, flag write/wait and event of the
+// round, so the host never limits a ring whose steps take tens of us.
+namespace g4 {
+struct RoundProgram {
+    std::vector<int64_t> ops;      // nops x G4_OP_WORDS
+    std::vector<void*> ptrs;       // staged payload pointer lists of K1/K3 ops
+    std::vector<int64_t> meta;     // K3: world_rank, lane, meas_base per payload
+    std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> events;
+    std::vector<cudaEvent_t> k1_ev;  // timing pairs per K1 op (timing programs only)
+    void* g4;
+    int64_t lo, hi, batch;
+    int32_t n, dtype, pdtype, mode;
+    uint64_t seed;
+    int n_acc;
+};
+}  // namespace g4
+
+extern "C" {
+
+g4_status g4_round_program_create(const int64_t* ops, int32_t nops, void* const* ptrs, int32_t nptrs,
+                                  const int64_t* meta, int32_t nmeta, void* const* streams, int32_t nstreams,
+                                  int32_t nevents, void* g4p, int64_t lo, int64_t hi, int32_t n, int32_t dtype,
+                                  int32_t pdtype, uint64_t seed, int32_t mode, int64_t batch, int32_t timing,
+                                  void** prog_out) {
+    using namespace g4;
+    if (!ops || nops < 1 || nptrs < 0 || nmeta < 0 || nstreams < 1 || !streams || nevents < 0 || !g4p ||
+        !prog_out || (nptrs && !ptrs) || (nmeta && !meta))
+        return fail(G4_ERR_CONTRACT, "round_program_create: bad arguments");
+    auto* P = new RoundProgram();
+    P->ops.assign(ops, ops + (size_t)nops * G4_OP_WORDS);
+    P->ptrs.assign(ptrs, ptrs + nptrs);
+    P->meta.assign(meta, meta + nmeta);
+    for (int i = 0; i < nstreams; ++i) P->streams.push_back(static_cast<cudaStream_t>(streams[i]));
+    P->g4 = g4p;
+    P->lo = lo;
+    P->hi = hi;
+    P->n = n;
+    P->dtype = dtype;
+    P->pdtype = pdtype;
+    P->seed = seed;
+    P->mode = mode;
+    P->batch = batch;
+    P->n_acc = 0;
+    for (int i = 0; i < nops; ++i) {
+        const int64_t* o = &P->ops[(size_t)i * G4_OP_WORDS];
+        const int64_t kind = o[0], st = o[1];
+        bool ok = st >= 0 && st < nstreams;
+        if (kind == G4_OP_ACC || kind == G4_OP_GEN) ok = ok && o[2] >= 0 && o[3] >= 1 && o[2] + o[3] <= nptrs;
+        if (kind == G4_OP_GEN) ok = ok && o[4] >= 0 && o[4] + 3 * o[3] <= nmeta;
+        if (kind == G4_OP_RECORD || kind == G4_OP_WAIT_EVENT) ok = ok && o[2] >= 0 && o[2] < nevents;
+        if (kind < G4_OP_ACC || kind > G4_OP_GEN) ok = false;
+        if (!ok) {
+            delete P;
+            set_error("round_program_create: malformed op %d (kind %lld)", i, (long long)kind);
+            return G4_ERR_CONTRACT;
+        }
+        if (kind == G4_OP_ACC) ++P->n_acc;
+    }
+    for (int i = 0; i < nevents; ++i) {
+        cudaEvent_t e;
+        cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+        if (err != cudaSuccess) {
+            g4_round_program_destroy(P);
+            return check_cuda(err, "cudaEventCreate");
+        }
+        P->events.push_back(e);
+    }
+    if (timing) {
+        for (int i = 0; i < 2 * P->n_acc; ++i) {
+            cudaEvent_t e;
+            cudaError_t err = cudaEventCreate(&e);
+            if (err != cudaSuccess) {
+                g4_round_program_destroy(P);
+                return check_cuda(err, "cudaEventCreate");
+            }
+            P->k1_ev.push_back(e);
+        }
+    }
+    *prog_out = P;
+    return G4_OK;
+}
+
+g4_status g4_round_program_run(void* prog, int64_t m, int32_t regenerate) {
+    using namespace g4;
+    auto* P = static_cast<RoundProgram*>(prog);
+    if (!P || m < 0) return fail(G4_ERR_CONTRACT, "round_program_run: bad arguments");
+    int acc = 0;
+    std::vector<int64_t> meas;
+    for (size_t i = 0; i < P->ops.size(); i += G4_OP_WORDS) {
+        const int64_t* o = &P->ops[i];
+        cudaStream_t st = P->streams[o[1]];
+        switch (o[0]) {
+            case G4_OP_GEN: {
+                if (!regenerate) break;
+                const int64_t cnt = o[3];
+                const int64_t* md = &P->meta[o[4]];
+                meas.resize(cnt);
+                for (int64_t j = 0; j < cnt; ++j) meas[j] = md[2 * cnt + j] + m * P->batch;
+                G4_TRY(g4_generate(&P->ptrs[o[2]], nullptr, nullptr, (int32_t)cnt, P->seed, md, md + cnt,
+                                   meas.data(), P->n, P->mode, P->pdtype, st));
+                break;
+            }
+            case G4_OP_ACC:
+                if (!P->k1_ev.empty()) G4_CUDA(cudaEventRecord(P->k1_ev[2 * acc], st));
+                G4_TRY(g4_accumulate_staged(P->g4, P->lo, P->hi, P->n, &P->ptrs[o[2]], (int32_t)o[3], P->dtype,
+                                            G4_CHANNEL_EQ1, st));
+                if (!P->k1_ev.empty()) G4_CUDA(cudaEventRecord(P->k1_ev[2 * acc + 1], st));
+                ++acc;
+                break;
+            case G4_OP_WAIT:
+                G4_TRY(g4_flag_wait(reinterpret_cast<void*>(o[2]), (uint64_t)(o[3] + o[4] * m), st));
+                break;
+            case G4_OP_WRITE:
+                G4_TRY(g4_flag_write(reinterpret_cast<void*>(o[2]), (uint64_t)(o[3] + o[4] * m), st));
+                break;
+            case G4_OP_COPY:
+                G4_TRY(g4_copy_async(reinterpret_cast<void*>(o[2]), reinterpret_cast<const void*>(o[3]), o[4], st));
+                break;
+            case G4_OP_RECORD:
+                G4_CUDA(cudaEventRecord(P->events[o[2]], st));
+                break;
+            case G4_OP_WAIT_EVENT:
+                G4_CUDA(cudaStreamWaitEvent(st, P->events[o[2]], 0));
+                break;
+            default:
+                return fail(G4_ERR_CONTRACT, "round_program_run: bad op");
+        }
+    }
+    return G4_OK;
+}
+
+g4_status g4_round_program_k1_ms(void* prog, double* mean_ms, int32_t* count) {
+    using namespace g4;
+    auto* P = static_cast<RoundProgram*>(prog);
+    if (!P || !mean_ms || !count) return fail(G4_ERR_CONTRACT, "round_program_k1_ms: bad arguments");
+    *count = 0;
+    *mean_ms = 0.0;
+    if (P->k1_ev.empty()) return fail(G4_ERR_CONTRACT, "round_program_k1_ms: program created without timing");
+    double sum = 0.0;
+    for (int i = 0; i < P->n_acc; ++i) {
+        float ms = 0.f;
+        G4_CUDA(cudaEventElapsedTime(&ms, P->k1_ev[2 * i], P->k1_ev[2 * i + 1]));
+        sum += ms;
+    }
+    *count = P->n_acc;
+    *mean_ms = P->n_acc ? sum / P->n_acc : 0.0;
+    return G4_OK;
+}
+
+g4_status g4_round_program_destroy(void* prog) {
+    auto* P = static_cast<g4::RoundProgram*>(prog);
+    if (!P) return G4_OK;
+    for (cudaEvent_t e : P->events) cudaEventDestroy(e);
+    for (cudaEvent_t e : P->k1_ev) cudaEventDestroy(e);
+    delete P;
     return G4_OK;
 }
 

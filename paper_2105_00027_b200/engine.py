@@ -272,6 +272,9 @@ class RingEngine:
         self.peers = PeerMap()
         self.kernel_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] | None = None
         self.next_round = 0
+        self._prog = None
+        self._prog_delta = None
+        self.native = self._native_ok()
         self._connect()
 
     # -- setup --------------------------------------------------------------
@@ -298,6 +301,9 @@ class RingEngine:
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
         self.sub.barrier()
+        if self._prog is not None:
+            self.lib.g4_round_program_destroy(self._prog)
+            self._prog = None
         self.peers.close()
 
     # -- helpers --------------------------------------------------------------
@@ -314,6 +320,117 @@ class RingEngine:
     def _flag_off(self, ci: int, flag: int) -> int:
         return (ci * S.FLAGS_PER_CHANNEL + flag) * 8
 
+    # -- native round program ---------------------------------------------------
+    def _native_ok(self) -> bool:
+        """Rounds are issued by the native program (one C call per round) unless
+        the run needs per-op host work: origin tracking, fault injection, a
+        truncated ring, or a partial last round.  G4RING_NATIVE=0 forces the
+        per-op host loop (A/B and parity tests)."""
+        cfg = self.cfg
+        return (os.environ.get("G4RING_NATIVE", "1") != "0" and not cfg.instrument and cfg.fault is None
+                and cfg.ring_steps_override is None and cfg.measurements % cfg.batch == 0)
+
+    def _program(self):
+        """Compile the round schedule (schedule.round_schedule) into the native
+        op list of g4_round_program_create.  Flag values are affine in the round
+        number; rounds 0 and 1 fix base and slope and round 2 checks them."""
+        if self._prog is not None:
+            return self._prog
+        cfg = self.cfg
+        rounds = [S.round_schedule(self.topo, self.pos, self.channels, m) for m in range(3)]
+        if not (len(rounds[0]) == len(rounds[1]) == len(rounds[2])):
+            raise ContractViolation("ring schedule is not round-invariant")
+        streams = [self.compute] + self.comm
+        sidx = lambda name: 0 if name == S.COMPUTE else 1 + int(name[4:])  # noqa: E731
+        ev_ids: dict[str, int] = {}
+        words, ptrs, meta = [], [], []
+        delta = {"acc": {t: 0 for t in range(cfg.lanes)}, "recv": {t: 0 for t in range(cfg.lanes)},
+                 "sent": {t: 0 for t in range(cfg.lanes)}, "msgs": {t: 0 for t in range(cfg.lanes)},
+                 "bytes": {t: 0 for t in range(cfg.lanes)}, "meas": 0}
+        nb = cfg.batch
+
+        def affine(i, pos):
+            a, b, c = (r[i][pos] for r in rounds)
+            if c - b != b - a:
+                raise ContractViolation("ring flag values are not affine in the round number")
+            return a, b - a
+
+        for i, op in enumerate(rounds[0]):
+            kind = op[0]
+            if any(r[i][0] != kind for r in rounds):
+                raise ContractViolation("ring schedule is not round-invariant")
+            if kind == "gen":
+                off, moff = len(ptrs), len(meta)
+                wr, ln, mb = [], [], []
+                for c in self.channels:
+                    for b in range(nb):
+                        for li, t in enumerate(c.lanes):
+                            ptrs.append(self._buf_ptr(c.index, S.GEN, b * len(c.lanes) + li))
+                            wr.append(self.world_rank)
+                            ln.append(t)
+                            mb.append(b)
+                meta += wr + ln + mb
+                words.append([_lib.G4_OP_GEN, 0, off, len(wr), moff, 0, 0, 0])
+            elif kind == "acc":
+                off = len(ptrs)
+                for ci, buf in op[1]:
+                    c = self.channels[ci]
+                    ptrs += [self._buf_ptr(ci, buf, j) for j in range(nb * len(c.lanes))]
+                    for t in c.lanes:
+                        delta["acc"][t] += nb
+                        if buf != S.GEN:
+                            delta["recv"][t] += nb
+                words.append([_lib.G4_OP_ACC, 0, off, len(ptrs) - off, 0, 0, 0, 0])
+                delta["meas"] += len(ptrs) - off
+            elif kind == "wait":
+                _, st, ci, flag, _ = op
+                base, slope = affine(i, 4)
+                words.append([_lib.G4_OP_WAIT, sidx(st), self.flags.data_ptr() + self._flag_off(ci, flag),
+                              base, slope, 0, 0, 0])
+            elif kind == "write":
+                _, st, peer, ci, flag, _ = op
+                base, slope = affine(i, 5)
+                words.append([_lib.G4_OP_WRITE, sidx(st), self.peer_flags[peer] + self._flag_off(ci, flag),
+                              base, slope, 0, 0, 0])
+            elif kind == "copy":
+                _, st, ci, src, peer, dst = op
+                c = self.channels[ci]
+                nbytes = nb * len(c.lanes) * self.payload_bytes
+                dst_ptr = self.peer_bufs[(peer, ci)] + dst * self.bufs[ci][0].numel() * self.bufs[ci].element_size()
+                words.append([_lib.G4_OP_COPY, sidx(st), dst_ptr, self._buf_ptr(ci, src), nbytes, 0, 0, 0])
+                for t in c.lanes:
+                    delta["sent"][t] += nb
+                    delta["msgs"][t] += 1
+                    delta["bytes"][t] += nbytes // len(c.lanes)
+            elif kind in ("record", "wait_event"):
+                eid = ev_ids.setdefault(op[2], len(ev_ids))
+                words.append([_lib.G4_OP_RECORD if kind == "record" else _lib.G4_OP_WAIT_EVENT,
+                              sidx(op[1]), eid, 0, 0, 0, 0, 0])
+            else:  # pragma: no cover
+                raise AssertionError(kind)
+        flat = [w for op in words for w in op]
+        prog = ctypes.c_void_p()
+        _lib.check(self.lib.g4_round_program_create(
+            _lib.i64_array(flat), len(words), _lib.ptr_array(ptrs), len(ptrs), _lib.i64_array(meta or [0]),
+            len(meta), _lib.ptr_array([st.cuda_stream for st in streams]), len(streams), len(ev_ids),
+            self.slice.data.data_ptr(), self.lo, self.hi, self.space.size, self.code, self.pcode,
+            cfg.seed & 0xFFFFFFFFFFFFFFFF, _MODE_CODE[cfg.value_mode], cfg.batch, 1, ctypes.byref(prog)),
+            "round_program_create")
+        self._prog, self._prog_delta = prog, delta
+        return prog
+
+    def k1_mean_ms(self) -> float:
+        """Mean K1 launch duration of the last completed round (native rounds),
+        or over the launches recorded in kernel_events (host-loop rounds)."""
+        if self._prog is not None:
+            mean, cnt = ctypes.c_double(), ctypes.c_int32()
+            _lib.check(self.lib.g4_round_program_k1_ms(self._prog, ctypes.byref(mean), ctypes.byref(cnt)),
+                       "round_program_k1_ms")
+            return mean.value
+        if not self.kernel_events:
+            raise ContractViolation("no K1 launches were timed")
+        return float(np.mean([a.elapsed_time(b) for a, b in self.kernel_events]))
+
     # -- one round ------------------------------------------------------------
     def enqueue_round(self, m: int | None = None, regenerate: bool = True) -> None:
         """Enqueue the next round (asynchronous).  Rounds must be consecutive:
@@ -326,6 +443,18 @@ class RingEngine:
             raise ContractViolation(f"rounds must be consecutive: expected {self.next_round}, got {m}")
         self.next_round = m + 1
         cfg = self.cfg
+        if self.native:
+            _lib.check(self.lib.g4_round_program_run(self._program(), m, int(regenerate)), "round_program_run")
+            d = self._prog_delta
+            for t, cnt in self.counters.items():
+                cnt.accumulations_applied += d["acc"][t]
+                cnt.envelopes_received += d["recv"][t]
+                cnt.envelopes_sent += d["sent"][t]
+                cnt.messages_sent += d["msgs"][t]
+                cnt.bytes_sent += d["bytes"][t]
+            self.slice.meas_count += d["meas"]
+            self.meas_count += d["meas"]
+            return
         nb = max(1, min(self._nb(m), cfg.batch)) if regenerate else cfg.batch
         fault = cfg.fault == "skip-send" and self.world_rank == 0 and m == 0
         ops = S.round_schedule(self.topo, self.pos, self.channels, m, cfg.ring_steps_override, fault)

@@ -141,3 +141,40 @@ def test_config_errors():
         E.validate_config(cfg(world_size=16, subring_size=16))  # more ranks than planes
     with pytest.raises(ConfigError):
         E.validate_config(cfg(lanes=1000))
+
+
+def check_counts(c, rep):
+    """Counter laws (C03) without origin tracking."""
+    s, k, m = c.subring_size, c.lanes, c.measurements
+    for r in range(c.world_size):
+        for t in range(k):
+            cnt = rep.lane_counters[(r, t)]
+            assert cnt["envelopes_sent"] == (s - 1) * m and cnt["envelopes_received"] == (s - 1) * m
+            assert cnt["accumulations_applied"] == s * m
+        assert rep.meas_counts[r] == s * m * k
+
+
+@pytest.mark.parametrize("kw", [
+    dict(world_size=2, subring_size=2, measurements=4, batch=2),
+    dict(world_size=4, subring_size=4, lanes=2, measurements=3),
+    dict(world_size=4, subring_size=2, lanes=2, measurements=4, batch=2),      # sub-rings + reduce
+    dict(world_size=3, subring_size=3, lanes=3, direction="alternate", n_w=3),
+    dict(world_size=4, subring_size=4, lanes=1, value_mode="float", n_k=8, n_w=16, planes=64, measurements=4, batch=4),
+])
+def test_native_round_program_matches_host_loop(kw, monkeypatch):
+    """The native round program (one C call per round) against the per-op host
+    loop on the same config: bitwise equal tensors (integer mode) or the same
+    float result, and the same counters."""
+    c = cfg(instrument=False, **kw)
+    monkeypatch.setenv("G4RING_NATIVE", "1")
+    native = E.run_experiment(c)
+    monkeypatch.setenv("G4RING_NATIVE", "0")
+    host = E.run_experiment(c)
+    ref = oracle_of(c)
+    if c.value_mode == "integer":
+        assert np.array_equal(native.tensor, ref) and np.array_equal(host.tensor, ref)
+    else:
+        assert np.array_equal(native.tensor, host.tensor)  # same walkers in the same order per entry
+        np.testing.assert_allclose(native.tensor, ref, rtol=1e-10, atol=1e-10 * np.abs(ref).max())
+    check_counts(c, native)
+    assert native.lane_counters == host.lane_counters

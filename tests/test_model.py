@@ -1,0 +1,111 @@
+"""Ring / K1 / memory models (paper_2105_00027_b200.model).
+
+* Parity: the reference closed forms (perf.py, memory.py) on the inputs
+  recorded from the real reference in tests/golden/models.json
+  (oracle/make_golden_models.py).
+* Calibration: the K1 model against this round's measured bench lines
+  (profiles/r01c_bench*.json, complex128).
+* B200 predictions: which BASELINE configs hide the ring on 8 GPUs.
+CPU only (the C library is used for host-side queries only)."""
+import json
+
+import pytest
+
+from paper_2105_00027_b200 import model as M
+from paper_2105_00027_b200.errors import ConfigError, ContractViolation
+
+from .conftest import GOLDEN, ROOT
+
+
+@pytest.fixture(scope="module")
+def gold():
+    return json.loads((GOLDEN / "models.json").read_text())
+
+
+def test_perf_closed_forms_match_reference(gold):
+    links = [M.LinkConfig(**d) for d in gold["links"]]
+    for row in gold["perf"]:
+        link = links[row["link"]]
+        assert list(M.slow_link(row["s"], link, row["lanes"])) == row["slow"]
+        assert M.predict_elapsed(row["s"], row["n_meas"], row["msg"], link, row["lanes"]) == pytest.approx(
+            row["predicted"], rel=1e-12)
+        assert M.model_utilization(row["s"], link, row["lanes"]) == pytest.approx(row["util"])
+    for s, want in gold["counts"].items():
+        assert list(M.message_counts(int(s))) == want
+
+
+def test_memory_plan_matches_reference(gold):
+    for case in gold["plans"]:
+        got = M.make_plan(*case["args"])
+        for k, v in case["plan"].items():
+            assert got[k] == pytest.approx(v, rel=1e-12), k
+    for total, p, want in gold["misc"]["slice_bytes"]:
+        assert M.slice_bytes(total, p) == want
+    for mode, k, mb, want in gold["misc"]["gsigma_total_bytes"]:
+        assert M.gsigma_total_bytes(mode, k, mb) == pytest.approx(want)
+
+
+def test_invalid_inputs():
+    with pytest.raises(ContractViolation):
+        M.message_counts(0)
+    with pytest.raises(ConfigError):
+        M.predict_elapsed(0, 1, 1, M.NVSWITCH_B200)
+    with pytest.raises(ConfigError):
+        M.LinkConfig(latency=0)
+    with pytest.raises(ConfigError):
+        M.device_plan(512, 64, 8, dtype="bf16")
+    with pytest.raises(ConfigError):
+        M.ring_round_time(6, 1, 512, 64, subring_size=4)
+
+
+def test_k1_model_against_measured_bench_lines():
+    """Within 15 % of every measured complex128 K1 line of this round (the
+    calibration's own data: B = 1 is HBM-bound, B = 8/16 smem-path-bound)."""
+    lines = sorted((ROOT / "profiles").glob("r01c_bench*.json"))
+    checked = 0
+    for f in lines:
+        d = json.loads(f.read_text())
+        c = d["config"]
+        if d["dtype"] != "c128" or c["planes"] < 16:   # P = 8 lines are host-launch-bound in bench.py
+            continue
+        k = M.k1_pass_time(c["n"], c["planes"], c["walkers_per_pass"], d["dtype"], d.get("arith", "exact"))
+        assert k["updates_per_s"] == pytest.approx(d["value"], rel=0.15), f.name
+        checked += 1
+    assert checked >= 4
+
+
+def test_k1_model_bounds_switch_with_batch():
+    assert M.k1_pass_time(512, 64, 1)["bound"] == "hbm"
+    assert M.k1_pass_time(512, 64, 16)["bound"] == "smem"
+
+
+def test_device_plan_and_max_g4():
+    p = M.device_plan(512, 64, 8, lanes=1, batch=8)
+    assert p["planes_per_gpu"] == 8
+    assert p["slice_bytes"] == 8 * 512 * 512 * 16
+    assert p["payload_bytes"] == 2 * 552 * 584 * 16
+    assert p["ring_buffer_bytes"] == 3 * 8 * p["payload_bytes"]
+    assert p["fits"]
+    c4 = M.device_plan(4608, 576, 8, batch=8)
+    assert c4["fits"] and c4["slice_bytes"] == 72 * 4608 ** 2 * 16
+    assert c4["g4_total_bytes"] > 180e9                 # config 4 does not fit one GPU ...
+    assert c4["max_g4_bytes"] > 6 * c4["g4_total_bytes"]  # ... and the node holds > 6x of it
+
+
+def test_ring_predictions_for_baseline_configs():
+    # config 4 (the paper's large case): 72 planes per GPU hide every ring step on 8 GPUs
+    r4 = M.ring_round_time(8, 8, 4608, 576, "c128")
+    assert r4["hidden"] and r4["compute_fraction"] > 0.95
+    # config 2 on 8 GPUs: 8 planes per GPU cannot hide a 10 MB payload per walker
+    r2 = M.ring_round_time(8, 8, 512, 64, "c128")
+    assert not r2["hidden"] and r2["transfer_s"] > 2 * r2["k1_s"]
+    # halving the payload (complex64 payloads) lowers the planes needed to hide the ring
+    assert M.hide_planes(512, 8, "mixed") < M.hide_planes(512, 8, "c128") <= 64
+    rows = M.scaling_table(4608, 576, 8, "c128")
+    assert [r["gpus"] for r in rows] == [1, 2, 4, 8] and rows[-1]["efficiency"] > 0.95
+
+
+def test_cli_runs(capsys):
+    M.main(["--config", "c2"])
+    out = capsys.readouterr().out
+    assert "c2 c128" in out and "ring-bound" in out
