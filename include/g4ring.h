@@ -199,13 +199,13 @@ g4_status g4_reduce_sum(void* dst, const void* const* src, int32_t nsrc, int64_t
  *   {G4_OP_GEN,   stream, ptr_off, count, meta_off}  K3 into ptrs with
  *       meta[meta_off ..] = world_rank[count], lane[count], meas_base[count];
  *       meas = meas_base + m * batch (skipped when regenerate == 0).
- * streams/ptrs are borrowed for the program's lifetime; events are owned. */
+ * streams, events and ptrs are borrowed for the program's lifetime. */
 #define G4_OP_WORDS 8
 enum { G4_OP_ACC = 1, G4_OP_WAIT = 2, G4_OP_WRITE = 3, G4_OP_COPY = 4, G4_OP_RECORD = 5,
        G4_OP_WAIT_EVENT = 6, G4_OP_GEN = 7 };
 g4_status g4_round_program_create(const int64_t* ops, int32_t nops, void* const* ptrs, int32_t nptrs,
                                   const int64_t* meta, int32_t nmeta, void* const* streams, int32_t nstreams,
-                                  int32_t nevents, void* g4, int64_t lo, int64_t hi, int32_t n, int32_t dtype,
+                                  void* const* events, int32_t nevents, void* g4, int64_t lo, int64_t hi, int32_t n, int32_t dtype,
                                   int32_t pdtype, uint64_t seed, int32_t mode, int64_t batch, int32_t timing,
                                   void** prog_out);
 g4_status g4_round_program_run(void* prog, int64_t m, int32_t regenerate);

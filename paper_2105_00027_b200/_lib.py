@@ -54,7 +54,7 @@ SIGNATURES = {
     "g4_flag_wait": (_i32, [_vp, _u64, _vp]),
     "g4_flag_host_wait": (_i32, [_vp, _u64, _i64]),
     "g4_reduce_sum": (_i32, [_vp, _vpp, _i32, _i64, _i32, _vp]),
-    "g4_round_program_create": (_i32, [_i64p, _i32, _vpp, _i32, _i64p, _i32, _vpp, _i32, _i32, _vp, _i64, _i64,
+    "g4_round_program_create": (_i32, [_i64p, _i32, _vpp, _i32, _i64p, _i32, _vpp, _i32, _vpp, _i32, _vp, _i64, _i64,
                                        _i32, _i32, _i32, _u64, _i32, _i64, _i32, _vpp]),
     "g4_round_program_run": (_i32, [_vp, _i64, _i32]),
     "g4_round_program_k1_ms": (_i32, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]),

@@ -238,8 +238,8 @@ struct RoundProgram {
     std::vector<void*> ptrs;       // staged payload pointer lists of K1/K3 ops
     std::vector<int64_t> meta;     // K3: world_rank, lane, meas_base per payload
     std::vector<cudaStream_t> streams;
-    std::vector<cudaEvent_t> events;
-    std::vector<cudaEvent_t> k1_ev;  // timing pairs per K1 op (timing programs only)
+    std::vector<cudaEvent_t> events;  // borrowed
+    std::vector<cudaEvent_t> k1_ev;   // timing pairs per K1 op (timing programs only; owned)
     void* g4;
     int64_t lo, hi, batch;
     int32_t n, dtype, pdtype, mode;
@@ -252,12 +252,12 @@ extern "C" {
 
 g4_status g4_round_program_create(const int64_t* ops, int32_t nops, void* const* ptrs, int32_t nptrs,
                                   const int64_t* meta, int32_t nmeta, void* const* streams, int32_t nstreams,
-                                  int32_t nevents, void* g4p, int64_t lo, int64_t hi, int32_t n, int32_t dtype,
+                                  void* const* events, int32_t nevents, void* g4p, int64_t lo, int64_t hi, int32_t n, int32_t dtype,
                                   int32_t pdtype, uint64_t seed, int32_t mode, int64_t batch, int32_t timing,
                                   void** prog_out) {
     using namespace g4;
     if (!ops || nops < 1 || nptrs < 0 || nmeta < 0 || nstreams < 1 || !streams || nevents < 0 || !g4p ||
-        !prog_out || (nptrs && !ptrs) || (nmeta && !meta))
+        !prog_out || (nptrs && !ptrs) || (nmeta && !meta) || (nevents && !events))
         return fail(G4_ERR_CONTRACT, "round_program_create: bad arguments");
     auto* P = new RoundProgram();
     P->ops.assign(ops, ops + (size_t)nops * G4_OP_WORDS);
@@ -290,13 +290,11 @@ g4_status g4_round_program_create(const int64_t* ops, int32_t nops, void* const*
         if (kind == G4_OP_ACC) ++P->n_acc;
     }
     for (int i = 0; i < nevents; ++i) {
-        cudaEvent_t e;
-        cudaError_t err = cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
-        if (err != cudaSuccess) {
-            g4_round_program_destroy(P);
-            return check_cuda(err, "cudaEventCreate");
+        if (!events[i]) {
+            delete P;
+            return fail(G4_ERR_CONTRACT, "round_program_create: null event");
         }
-        P->events.push_back(e);
+        P->events.push_back(static_cast<cudaEvent_t>(events[i]));
     }
     if (timing) {
         for (int i = 0; i < 2 * P->n_acc; ++i) {
@@ -383,7 +381,6 @@ g4_status g4_round_program_k1_ms(void* prog, double* mean_ms, int32_t* count) {
 g4_status g4_round_program_destroy(void* prog) {
     auto* P = static_cast<g4::RoundProgram*>(prog);
     if (!P) return G4_OK;
-    for (cudaEvent_t e : P->events) cudaEventDestroy(e);
     for (cudaEvent_t e : P->k1_ev) cudaEventDestroy(e);
     delete P;
     return G4_OK;

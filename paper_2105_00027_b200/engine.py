@@ -272,9 +272,10 @@ class RingEngine:
         self.peers = PeerMap()
         self.kernel_events: list[tuple[torch.cuda.Event, torch.cuda.Event]] | None = None
         self.next_round = 0
-        self._prog = None
+        self._prog = [None, None]  # native round programs by round parity
         self._prog_delta = None
         self.native = self._native_ok()
+        self._make_events()
         self._connect()
 
     # -- setup --------------------------------------------------------------
@@ -301,9 +302,10 @@ class RingEngine:
     def close(self) -> None:
         torch.cuda.synchronize(self.device)
         self.sub.barrier()
-        if self._prog is not None:
-            self.lib.g4_round_program_destroy(self._prog)
-            self._prog = None
+        for i, prog in enumerate(self._prog):
+            if prog is not None:
+                self.lib.g4_round_program_destroy(prog)
+                self._prog[i] = None
         self.peers.close()
 
     # -- helpers --------------------------------------------------------------
@@ -330,35 +332,29 @@ class RingEngine:
         return (os.environ.get("G4RING_NATIVE", "1") != "0" and not cfg.instrument and cfg.fault is None
                 and cfg.ring_steps_override is None and cfg.measurements % cfg.batch == 0)
 
-    def _program(self):
-        """Compile the round schedule (schedule.round_schedule) into the native
-        op list of g4_round_program_create.  Flag values are affine in the round
-        number; rounds 0 and 1 fix base and slope and round 2 checks them."""
-        if self._prog is not None:
-            return self._prog
+    NATIVE_FROM_ROUND = S.STEADY_FROM_ROUND
+
+    def _program(self, m: int):
+        """Compile the steady-state schedule of round parity m % 2
+        (schedule.steady_state_template: flag values affine in the round
+        number) into the native op list of g4_round_program_create.  Rounds 0
+        and 1 run the host loop; stream events are shared with it."""
+        par = m % 2
+        if self._prog[par] is not None:
+            return self._prog[par]
         cfg = self.cfg
-        rounds = [S.round_schedule(self.topo, self.pos, self.channels, m) for m in range(3)]
-        if not (len(rounds[0]) == len(rounds[1]) == len(rounds[2])):
-            raise ContractViolation("ring schedule is not round-invariant")
+        template = S.steady_state_template(self.topo, self.pos, self.channels, par)
         streams = [self.compute] + self.comm
         sidx = lambda name: 0 if name == S.COMPUTE else 1 + int(name[4:])  # noqa: E731
-        ev_ids: dict[str, int] = {}
+        ev_names = list(self.events)
         words, ptrs, meta = [], [], []
-        delta = {"acc": {t: 0 for t in range(cfg.lanes)}, "recv": {t: 0 for t in range(cfg.lanes)},
-                 "sent": {t: 0 for t in range(cfg.lanes)}, "msgs": {t: 0 for t in range(cfg.lanes)},
-                 "bytes": {t: 0 for t in range(cfg.lanes)}, "meas": 0}
+        lanes = range(cfg.lanes)
+        delta = {"acc": dict.fromkeys(lanes, 0), "recv": dict.fromkeys(lanes, 0), "sent": dict.fromkeys(lanes, 0),
+                 "msgs": dict.fromkeys(lanes, 0), "bytes": dict.fromkeys(lanes, 0), "meas": 0}
         nb = cfg.batch
 
-        def affine(i, pos):
-            a, b, c = (r[i][pos] for r in rounds)
-            if c - b != b - a:
-                raise ContractViolation("ring flag values are not affine in the round number")
-            return a, b - a
-
-        for i, op in enumerate(rounds[0]):
+        for op in template:
             kind = op[0]
-            if any(r[i][0] != kind for r in rounds):
-                raise ContractViolation("ring schedule is not round-invariant")
             if kind == "gen":
                 off, moff = len(ptrs), len(meta)
                 wr, ln, mb = [], [], []
@@ -383,13 +379,11 @@ class RingEngine:
                 words.append([_lib.G4_OP_ACC, 0, off, len(ptrs) - off, 0, 0, 0, 0])
                 delta["meas"] += len(ptrs) - off
             elif kind == "wait":
-                _, st, ci, flag, _ = op
-                base, slope = affine(i, 4)
+                _, st, ci, flag, base, slope = op
                 words.append([_lib.G4_OP_WAIT, sidx(st), self.flags.data_ptr() + self._flag_off(ci, flag),
                               base, slope, 0, 0, 0])
             elif kind == "write":
-                _, st, peer, ci, flag, _ = op
-                base, slope = affine(i, 5)
+                _, st, peer, ci, flag, base, slope = op
                 words.append([_lib.G4_OP_WRITE, sidx(st), self.peer_flags[peer] + self._flag_off(ci, flag),
                               base, slope, 0, 0, 0])
             elif kind == "copy":
@@ -403,28 +397,43 @@ class RingEngine:
                     delta["msgs"][t] += 1
                     delta["bytes"][t] += nbytes // len(c.lanes)
             elif kind in ("record", "wait_event"):
-                eid = ev_ids.setdefault(op[2], len(ev_ids))
                 words.append([_lib.G4_OP_RECORD if kind == "record" else _lib.G4_OP_WAIT_EVENT,
-                              sidx(op[1]), eid, 0, 0, 0, 0, 0])
+                              sidx(op[1]), ev_names.index(op[2]), 0, 0, 0, 0, 0])
             else:  # pragma: no cover
                 raise AssertionError(kind)
         flat = [w for op in words for w in op]
         prog = ctypes.c_void_p()
         _lib.check(self.lib.g4_round_program_create(
             _lib.i64_array(flat), len(words), _lib.ptr_array(ptrs), len(ptrs), _lib.i64_array(meta or [0]),
-            len(meta), _lib.ptr_array([st.cuda_stream for st in streams]), len(streams), len(ev_ids),
+            len(meta), _lib.ptr_array([st.cuda_stream for st in streams]), len(streams),
+            _lib.ptr_array([self.events[k].cuda_event for k in ev_names]), len(ev_names),
             self.slice.data.data_ptr(), self.lo, self.hi, self.space.size, self.code, self.pcode,
             cfg.seed & 0xFFFFFFFFFFFFFFFF, _MODE_CODE[cfg.value_mode], cfg.batch, 1, ctypes.byref(prog)),
             "round_program_create")
-        self._prog, self._prog_delta = prog, delta
+        self._prog[par], self._prog_delta = prog, delta
         return prog
+
+    def _make_events(self) -> None:
+        """Create every named stream event of the schedule up front (recorded
+        once so the CUDA event exists), shared by host-loop and native rounds."""
+        names = []
+        for m in range(4):
+            for op in S.round_schedule(self.topo, self.pos, self.channels, m):
+                if op[0] in ("record", "wait_event") and op[2] not in names:
+                    names.append(op[2])
+        for name in names:
+            ev = torch.cuda.Event()
+            ev.record(self.compute)
+            self.events[name] = ev
+        self.compute.synchronize()
 
     def k1_mean_ms(self) -> float:
         """Mean K1 launch duration of the last completed round (native rounds),
         or over the launches recorded in kernel_events (host-loop rounds)."""
-        if self._prog is not None:
+        last = (self.next_round - 1) % 2
+        if self.native and self.next_round > self.NATIVE_FROM_ROUND and self._prog[last] is not None:
             mean, cnt = ctypes.c_double(), ctypes.c_int32()
-            _lib.check(self.lib.g4_round_program_k1_ms(self._prog, ctypes.byref(mean), ctypes.byref(cnt)),
+            _lib.check(self.lib.g4_round_program_k1_ms(self._prog[last], ctypes.byref(mean), ctypes.byref(cnt)),
                        "round_program_k1_ms")
             return mean.value
         if not self.kernel_events:
@@ -443,8 +452,8 @@ class RingEngine:
             raise ContractViolation(f"rounds must be consecutive: expected {self.next_round}, got {m}")
         self.next_round = m + 1
         cfg = self.cfg
-        if self.native:
-            _lib.check(self.lib.g4_round_program_run(self._program(), m, int(regenerate)), "round_program_run")
+        if self.native and m >= self.NATIVE_FROM_ROUND:
+            _lib.check(self.lib.g4_round_program_run(self._program(m), m, int(regenerate)), "round_program_run")
             d = self._prog_delta
             for t, cnt in self.counters.items():
                 cnt.accumulations_applied += d["acc"][t]
@@ -526,12 +535,9 @@ class RingEngine:
                     self.counters[t].messages_sent += 1
                     self.counters[t].bytes_sent += nbytes // len(c.lanes)
             elif kind == "record":
-                ev = self.events.setdefault(op[2], torch.cuda.Event())
-                ev.record(self._stream(op[1]))
+                self.events[op[2]].record(self._stream(op[1]))
             elif kind == "wait_event":
-                ev = self.events.get(op[2])
-                if ev is not None:
-                    self._stream(op[1]).wait_event(ev)
+                self._stream(op[1]).wait_event(self.events[op[2]])
             else:  # pragma: no cover
                 raise AssertionError(kind)
 

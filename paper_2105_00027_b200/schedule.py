@@ -180,3 +180,39 @@ def round_schedule(topo: RingTopology, pos: int, channels: list[Channel], m: int
         for c in channels:
             ops.append(("write", COMPUTE, c.recv_from, c.index, ACK_ACC, k))
     return ops
+
+
+# Rounds 0 and 1 lack the slot-reuse waits of the steady state (their receive
+# slots were never used before); from round 2 on, the schedule repeats with
+# period 2 (a transfer's receive slot alternates with its index) and every
+# flag value is affine in the round number.
+STEADY_FROM_ROUND = 2
+
+
+def steady_state_template(topo: RingTopology, pos: int, channels: list[Channel],
+                          parity: int) -> list[tuple]:
+    """The round schedule for every round m >= STEADY_FROM_ROUND with m % 2 ==
+    parity, as one op list whose flag ops ("wait", "write") end in the pair
+    (base, slope) such that the value of round m is base + slope * m.  The
+    instrumentation tag of "acc" ops is dropped; "gen" ops keep no round index.
+    Raises ContractViolation if the schedule is not periodic."""
+    t0 = STEADY_FROM_ROUND + ((parity - STEADY_FROM_ROUND) % 2)
+    rounds = [round_schedule(topo, pos, channels, t0 + 2 * i) for i in range(3)]
+    if not len(rounds[0]) == len(rounds[1]) == len(rounds[2]):
+        raise ContractViolation("ring schedule is not periodic in the round number")
+    out = []
+    for i, op in enumerate(rounds[0]):
+        kind = op[0]
+        key = {"acc": lambda o: o[:2], "gen": lambda o: o[:1],
+               "wait": lambda o: o[:-1], "write": lambda o: o[:-1]}.get(kind, lambda o: o)
+        if any(r[i][0] != kind or key(r[i]) != key(op) for r in rounds[1:]):
+            raise ContractViolation("ring schedule is not periodic in the round number")
+        if kind in ("wait", "write"):
+            a, b, c = (r[i][-1] for r in rounds)
+            if c - b != b - a or (b - a) % 2:
+                raise ContractViolation("ring flag values are not affine in the round number")
+            slope = (b - a) // 2
+            out.append(op[:-1] + (a - slope * t0, slope))
+        else:
+            out.append(key(op))
+    return out

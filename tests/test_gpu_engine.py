@@ -155,15 +155,17 @@ def check_counts(c, rep):
 
 
 @pytest.mark.parametrize("kw", [
-    dict(world_size=2, subring_size=2, measurements=4, batch=2),
-    dict(world_size=4, subring_size=4, lanes=2, measurements=3),
-    dict(world_size=4, subring_size=2, lanes=2, measurements=4, batch=2),      # sub-rings + reduce
-    dict(world_size=3, subring_size=3, lanes=3, direction="alternate", n_w=3),
-    dict(world_size=4, subring_size=4, lanes=1, value_mode="float", n_k=8, n_w=16, planes=64, measurements=4, batch=4),
+    dict(world_size=2, subring_size=2, measurements=8, batch=2),
+    dict(world_size=4, subring_size=4, lanes=2, measurements=5),
+    dict(world_size=4, subring_size=2, lanes=2, measurements=8, batch=2),      # sub-rings + reduce
+    dict(world_size=3, subring_size=3, lanes=3, direction="alternate", n_w=3, measurements=5),
+    dict(world_size=4, subring_size=4, lanes=1, value_mode="float", n_k=8, n_w=16, planes=64, measurements=16,
+         batch=4),
 ])
 def test_native_round_program_matches_host_loop(kw, monkeypatch):
-    """The native round program (one C call per round) against the per-op host
-    loop on the same config: bitwise equal tensors (integer mode) or the same
+    """The native round program (one C call per round from round 2 on) against
+    the per-op host loop on the same config (>= 4 rounds, so both round
+    parities run natively): bitwise equal tensors (integer mode) or the same
     float result, and the same counters."""
     c = cfg(instrument=False, **kw)
     monkeypatch.setenv("G4RING_NATIVE", "1")

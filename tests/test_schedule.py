@@ -149,3 +149,29 @@ def test_payload_ends_left_of_birth_rank():
         k_last = S.transfer_index(0, 2, 4)
         last = st.bufs[(0, S.R0 + k_last % 2)]
         assert last[0]["origin"][1] == (st.pos + 1) % 4
+
+
+@pytest.mark.parametrize("world,s,lanes,direction", [(2, 2, 1, "forward"), (4, 4, 2, "forward"),
+                                                     (4, 2, 2, "forward"), (3, 3, 3, "alternate"),
+                                                     (8, 8, 1, "forward"), (8, 4, 2, "alternate")])
+def test_steady_state_template_reproduces_rounds(world, s, lanes, direction):
+    """The native round program's template (period 2, flag values affine in m)
+    reproduces round_schedule for every steady-state round."""
+    topo = S.RingTopology(world, s, lanes, direction)
+    for pos in range(s):
+        ch = S.make_channels(topo, pos)
+        for par in (0, 1):
+            tpl = S.steady_state_template(topo, pos, ch, par)
+            for m in range(S.STEADY_FROM_ROUND, 12):
+                if m % 2 != par:
+                    continue
+                got = S.round_schedule(topo, pos, ch, m)
+                assert len(got) == len(tpl)
+                for t, r in zip(tpl, got):
+                    assert t[0] == r[0]
+                    if t[0] in ("wait", "write"):
+                        assert t[:-2] == r[:-1] and t[-2] + t[-1] * m == r[-1]
+                    elif t[0] == "acc":
+                        assert t == r[:2]
+                    elif t[0] != "gen":
+                        assert t == r
