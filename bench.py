@@ -292,7 +292,7 @@ def run_gpu(args):
                    else "slice fits L2 (L2-resident caveat)"},
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None,
+                     "frac": achieved / peak, "traffic": k1_traffic(lib, n, planes, B, args.dtype, args.arith),
                      "peak_source": peak_kind, "kernel": "k_accumulate",
                      "bytes_per_launch": alg_bytes},
         "onchip": onchip_bounds(lib, n, planes, args.dtype, args.arith, B, upd_step / (statistics.mean(k_ms) * 1e-3)),
@@ -312,6 +312,21 @@ def run_gpu(args):
                       f"numpy port of accumulate_g4 in {used} processes on disjoint K3 ranges; "
                       f"host {cpu_model()}"}
     print(json.dumps(line), flush=True)
+
+
+def k1_traffic(lib, n, planes, B, dtype, arith):
+    """DRAM bytes per K1 launch from the committed ncu capture of this exact
+    launch configuration (profiles/k1_traffic.json), else None."""
+    import ctypes
+    cfg = (ctypes.c_int32 * 8)()
+    lib.g4_k1_config(n, planes, {"c128": 0, "c64": 1, "mixed": 2}[dtype], cfg)
+    v = list(cfg)
+    key = f"v{v[0]}/{v[1]}x{v[2]}/{v[3]}x{v[4]}/{v[5]} n={n} planes={planes} B={B} {dtype} {arith}"
+    try:
+        d = json.loads((ROOT / "profiles" / "k1_traffic.json").read_text()).get(key)
+    except (OSError, ValueError):
+        return None
+    return None if d is None else d["dram_read_bytes"] + d["dram_write_bytes"]
 
 
 # On-chip ceilings of K1 (calibrated with tools/microbench.cu, profiles/r01_microbench.txt):
