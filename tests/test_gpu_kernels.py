@@ -218,7 +218,8 @@ def test_contract_violations(cuda_dev):
 
 
 @pytest.mark.parametrize("n,lo,hi,variant", [(48, 10, 18, 0), (160, 5, 40, 0), (160, 5, 40, 1),
-                                             (257, 240, 257, 2), (96, 0, 96, 2)])
+                                             (257, 240, 257, 2), (96, 0, 96, 2),
+                                             (160, 3, 11, 0), (129, 120, 129, 0), (512, 0, 4, 0)])
 def test_complex64(oracle, cuda_dev, n, lo, hi, variant):
     lib = _lib.load()
     _lib.check(lib.g4_set_kernel_variant(variant))
@@ -327,7 +328,8 @@ def test_fused_arith_within_tolerance(oracle, cuda_dev, variant):
         _lib.check(lib.g4_set_kernel_variant(0))
 
 
-@pytest.mark.parametrize("n,lo,hi,variant", [(40, 3, 9, 0), (128, 0, 40, 0), (128, 0, 40, 1), (161, 150, 161, 2)])
+@pytest.mark.parametrize("n,lo,hi,variant", [(40, 3, 9, 0), (128, 0, 40, 0), (128, 0, 40, 1), (161, 150, 161, 2),
+                                             (161, 150, 161, 0), (96, 7, 15, 0)])
 def test_mixed_precision_bitwise(oracle, cuda_dev, n, lo, hi, variant):
     """complex128 G4 with complex64 payloads: bitwise equal to the complex128
     reference applied to the complex64-rounded payloads (widening is exact)."""
