@@ -311,14 +311,12 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
     int32_t nx;   // plane chunks
     int32_t off;  // sheared-coordinate offset (elements), see make_maps
-    int32_t ahead;  // CTAs resident on the whole GPU (L2 prefetch distance)
 };
 
 // Measurement-only variants of K1 v2 (G4RING_EXP, never set in production):
 //   1 = start from zero accumulators (no G4 read)   2 = no G4 write
-//   4 = no shared-memory reads / math                8 = L2-prefetch the G4 tile
-//       of the CTA one resident wave ahead
-enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, EXP_PREFETCH = 8 };
+//   4 = no shared-memory reads / math  (bits combine; profiles/r01_summary.md)
+enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4 };
 static int exp_flags() {
     static int e = -1;
     if (e < 0) {
@@ -391,27 +389,6 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int w = 0; w < NST && w < P.nbatch; ++w) issue(w);
-    }
-    if constexpr ((EXP & EXP_PREFETCH) != 0) {
-        // warp 1: the G4 rows of the CTA one resident wave ahead -> L2
-        const unsigned nb = blockIdx.x + (unsigned)P.ahead;
-        if (warp == 1 && nb < gridDim.x) {
-            const TileCoord t2 = tile_coord(nb, P.nx, (n + 31) / 32, (n + DR - 1) / DR);
-            const int64_t qa = P.lo + (int64_t)t2.x * Q;
-#pragma unroll 1
-            for (int i = 0; i < (Q * DR + 31) / 32; ++i) {
-                const int r = lane + 32 * i;  // (plane, row) pair
-                const int64_t q = qa + r / DR;
-                const int k1 = t2.z * DR + r % DR;
-                if (r < Q * DR && q < P.hi && k1 < n) {
-                    const int c0 = t2.y * 32 + r % DR;
-                    const int len = min(32, n - c0);
-                    const Cx<R>* a = P.g4 + ((q - P.lo) * n + k1) * (int64_t)n + c0;
-                    const uint32_t bytes = (uint32_t)(len * sizeof(Cx<R>)) & ~15u;
-                    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a), "r"(bytes) : "memory");
-                }
-            }
-        }
     }
     __syncthreads();
 
@@ -590,16 +567,9 @@ static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, in
 template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
 static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     static bool attr_set = false;
-    static int ahead = 0;
     if (!attr_set) {
         G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-        int dev = 0, sms = 0, per_sm = 0;
-        G4_CUDA(cudaGetDevice(&dev));
-        G4_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        G4_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
-                                                              32 * G::CW, G::SMEM));
-        ahead = sms * std::max(per_sm, 1);
         attr_set = true;
     }
     const int n = prm.n;
@@ -611,7 +581,6 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
         tp.hi = prm.hi;
         tp.n = n;
         tp.off = sheared_offset(n, G::ES);
-        tp.ahead = ahead;
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
@@ -642,23 +611,24 @@ template <typename R, typename RG, bool FUSED>
 static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
     switch (g) {
         case 0: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3>, FUSED, 3>(prm, st);
-        case 3:
-            if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
-                switch (exp_flags()) {  // measurement variants (complex128 only)
-                    case 0: break;
-                    case 3: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 3>(prm, st);
-                    case 4: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 4>(prm, st);
-                    case 7: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 7>(prm, st);
-                    case 8: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4, 8>(prm, st);
-                    default: return fail(G4_ERR_CONTRACT, "G4RING_EXP: unknown variant");
-                }
-            }
-            return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
+        case 3: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
         case 7: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 2>, FUSED, 2>(prm, st);
         case 8: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2, 4, 4>, FUSED, 1>(prm, st);
         case 11: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3, 4, 2>, FUSED, 2>(prm, st);
         case 12: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2>, FUSED, 2>(prm, st);
-        case 13: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4>(prm, st);
+        case 13:
+            if constexpr (sizeof(R) == 8 && sizeof(RG) == 8) {
+                switch (exp_flags()) {  // measurement variants (complex128 only)
+                    case 0: break;
+                    case 1: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4, 1>(prm, st);
+                    case 2: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4, 2>(prm, st);
+                    case 3: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4, 3>(prm, st);
+                    case 4: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4, 4>(prm, st);
+                    case 7: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4, 7>(prm, st);
+                    default: return fail(G4_ERR_CONTRACT, "G4RING_EXP: unknown variant");
+                }
+            }
+            return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4>(prm, st);
         case 16: return launch_v2<R, RG, V2Geom<RG, 4, 4, 4>, FUSED, 2>(prm, st);
         case 17: return launch_v2<R, RG, V2Geom<RG, 8, 2, 4, 2, 2>, FUSED, 2>(prm, st);
         case 19: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4>(prm, st);
