@@ -165,8 +165,18 @@ g4_status g4_flag_wait(const void* flag, uint64_t value, void* stream) {
     static PFN_wait64 fn = nullptr;
     if (!flag || !aligned(flag, 8)) return fail(G4_ERR_CONTRACT, "flag_wait: bad flag pointer");
     if (!fn) G4_TRY(driver_fn("cuStreamWaitValue64", reinterpret_cast<void**>(&fn)));
-    CUresult r = fn(static_cast<CUstream>(stream), (CUdeviceptr)flag, (cuuint64_t)value,
-                    CU_STREAM_WAIT_VALUE_GEQ);
+    // Where the device supports it, the wait also flushes outstanding remote
+    // (NVLink peer) writes, so the payload that the flag announces is visible
+    // to the K1 launch that follows on this stream.
+    static int flush = -1;
+    if (flush < 0) {
+        int dev = 0, v = 0;
+        flush = (cudaGetDevice(&dev) == cudaSuccess &&
+                 cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev) == cudaSuccess && v)
+                    ? 1 : 0;
+    }
+    const unsigned int how = CU_STREAM_WAIT_VALUE_GEQ | (flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
+    CUresult r = fn(static_cast<CUstream>(stream), (CUdeviceptr)flag, (cuuint64_t)value, how);
     if (r != CUDA_SUCCESS) {
         set_error("cuStreamWaitValue64 failed (CUresult %d)", (int)r);
         return G4_ERR_TRANSPORT;
