@@ -517,13 +517,16 @@ def run_ring(args):
     rank, n_ranks = world.rank, world.size
     n_k, n_w, planes, desc = CONFIGS[args.config]
     B = args.batch
-    cfg = E.ExperimentConfig(n_k=n_k, n_w=n_w, world_size=n_ranks, subring_size=n_ranks, lanes=1,
+    # BASELINE config 3 is 8 GPUs as 2 sub-rings of 4 with 2 walker streams (lanes) per GPU
+    S = args.subring_size or (min(4, n_ranks) if args.config == "c3" else n_ranks)
+    lanes = args.lanes or (2 if args.config == "c3" else 1)
+    cfg = E.ExperimentConfig(n_k=n_k, n_w=n_w, world_size=n_ranks, subring_size=S, lanes=lanes,
                              measurements=B, seed=0, value_mode="float", planes=planes, batch=B,
                              dtype=args.dtype, gather=False, instrument=False, timeout_s=120.0)
     E.validate_config(cfg)
     dev = E.device_for_rank(rank)
     torch.cuda.set_device(dev)
-    sub = E.build_subrings(world, n_ranks)
+    sub = E.build_subrings(world, S)
     eng = E.RingEngine(cfg, sub, rank, dev)
     n = eng.space.size
     eb = 16 if args.dtype == "c128" else 8
@@ -560,22 +563,24 @@ def run_ring(args):
         return
     ms = max(x["ms"] for x in stats)
     kms = max(x["k_ms"] for x in stats)
-    upd_step = n_ranks * B * planes * n * n
+    # every rank applies the S x B x lanes payloads of its sub-ring to planes / S planes
+    upd_step = n_ranks * B * lanes * planes * n * n
     value = upd_step / (ms * 1e-3)
     p_local = max(x["hi"] - x["lo"] for x in stats)
     peak, peak_kind = measured_peaks()
-    # one K1 launch applies B walkers to the rank's p_local planes
-    alg_bytes = 2 * p_local * n * n * eb + B * 2 * n * n * eb
+    # one K1 launch applies B x lanes walkers to the rank's p_local planes
+    peb = 16 if args.dtype == "c128" else 8
+    alg_bytes = 2 * p_local * n * n * eb + B * lanes * 2 * n * n * peb
     achieved = alg_bytes / (kms * 1e-3) / 1e9
-    ring_bytes = (n_ranks - 1) * B * eng.payload_bytes
+    ring_bytes = (S - 1) * B * lanes * eng.payload_bytes
     line = {
         "metric": "G4 updates/s", "value": value, "unit": "updates/s", "n_gpus": n_ranks,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
         "data": "synthetic (reference counter-based generator on device, float mode, seed 0; resident)",
         "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
-                   "planes_per_gpu": p_local, "walkers_per_rank_per_step": B, "subring_size": n_ranks,
-                   "lanes": 1, "parallelism": f"ring{n_ranks}",
+                   "planes_per_gpu": p_local, "walkers_per_rank_per_step": B, "subring_size": S,
+                   "lanes": lanes, "parallelism": f"{n_ranks // S} sub-ring(s) of {S}",
                    "devices": torch.cuda.device_count()},
         "per_gpu_updates_per_s": value / n_ranks,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -589,16 +594,16 @@ def run_ring(args):
         "host": {"enqueue_ms_per_step": max(x["host_ms"] for x in stats),
                  "native_rounds": eng_native,
                  "note": "host time to issue one round (one C call with the native round program)"},
-        "model": ring_model_line(n, planes, n_ranks, B, args.dtype),
-        "gpu_launches": args.steps * n_ranks,  # K1 launches per rank per step = S (own + S-1 received)
+        "model": ring_model_line(n, planes, n_ranks, B, args.dtype, S, lanes),
+        "gpu_launches": args.steps * S,  # K1 launches per rank per step = S (own + S-1 received)
     }
     print(json.dumps(line), flush=True)
 
 
-def ring_model_line(n, planes, gpus, batch, dtype):
+def ring_model_line(n, planes, gpus, batch, dtype, subring_size, lanes):
     """The NVLink-5 ring model's prediction for this run (paper_2105_00027_b200.model)."""
     from paper_2105_00027_b200 import model as M
-    r = M.ring_round_time(gpus, batch, n, planes, dtype)
+    r = M.ring_round_time(gpus, batch, n, planes, dtype, lanes, subring_size)
     return {"round_ms": r["round_s"] * 1e3, "k1_ms": r["k1_s"] * 1e3, "step_transfer_ms": r["transfer_s"] * 1e3,
             "ring_hidden": r["hidden"], "updates_per_s": r["updates_per_s"],
             "hide_from_planes_per_gpu": M.hide_planes(n, batch, dtype),
@@ -609,7 +614,7 @@ def run_ring_e2e(args, eng, world, dev):
     """Ring e2e: each rank's walkers arrive in pinned host memory (reference
     layout); per step H2D + stage (K2) + round + D2H of a probe row."""
     import torch
-    B = args.batch
+    B = args.batch * eng.cfg.lanes  # walkers staged per rank per round (all lanes)
     n = eng.space.size
     dtype = eng.dtype
     ups = [torch.randn(n, n, dtype=dtype).pin_memory() for _ in range(B)]
@@ -642,7 +647,7 @@ def run_ring_e2e(args, eng, world, dev):
     torch.cuda.synchronize(dev)
     ms = max(world.allgather(t0.elapsed_time(t1) / args.steps))
     eb = 16 if dtype == torch.complex128 else 8
-    return {"value": world.size * B * eng.cfg.num_planes * n * n / (ms * 1e-3),
+    return {"value": world.size * B * eng.cfg.num_planes * n * n / (ms * 1e-3),  # B includes lanes
             "unit": "updates/s", "h2d_bytes_per_step": B * 2 * n * n * eb, "d2h_bytes_per_step": n * eb,
             "path": "pinned host walkers -> H2D -> g4_prepare_g (K2) -> ring round; D2H probe row"}
 
@@ -663,6 +668,8 @@ def main():
     ap.add_argument("--planes", type=int, default=0, help="override the exchange-plane count (N=1)")
     ap.add_argument("--max-g4", action="store_true", help="allocate + update + verify the largest N=4608 slice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--subring-size", type=int, default=0, help="ring size S for N > 1 (default N; c3: 4)")
+    ap.add_argument("--lanes", type=int, default=0, help="walker streams per GPU for N > 1 (default 1; c3: 2)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
