@@ -192,7 +192,7 @@ def run_reference(args):
     rate, step_s, used = cpu_throughput(n, planes, walkers, args.steps, args.warmup, cores)
     line = {
         "metric": "G4 updates/s", "value": rate, "unit": "updates/s", "impl": "reference",
-        "n_gpus": 0, "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
+        "n_gpus": args.gpus, "device": "cpu (all host cores; the same work at every N)", "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (reference generator, float mode, seed 0)",
         "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
