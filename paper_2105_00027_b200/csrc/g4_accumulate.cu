@@ -9,27 +9,30 @@
 //   p1 = S.u * D.d ; p2 = S.d * D.u ; t = p1 + p2 ; G += t
 // -- the reference's exact op order (tensor.py:250: u*down + d*up, then +=).
 //
-// Register block (both kernels): one thread owns PP x DD = 4 x 4 G4 entries:
-// planes q0..q0+3 x the diagonal (k1_0 + d, c + d), d < 4.  The shifted index
-// (q-k1, q-k2) then depends only on m = p - d, so the 16 updates of one walker
-// need 4 direct + 7 shifted staged elements.  A warp's 32 lanes own 32
-// consecutive k2 columns: G4 rows are read/written as contiguous 512 B runs,
-// staged rows as contiguous (forward or reversed) runs.  The G4 block is read
-// once, receives every walker of the batch in order (bitwise identical to
-// sequential reference calls), and is written once: HBM traffic per pass is
+// Register block: one thread owns PP x DD G4 entries, planes q0..q0+PP-1 x the
+// diagonal (k1_0 + d, c + d), d < DD (v1: 4 x 4; v2 default: 8 x 2).  The
+// shifted index (q-k1, q-k2) then depends only on m = p - d, so the PP*DD
+// updates of one walker need DD direct + PP+DD-1 shifted staged elements (16
+// updates from 11 for both blocks).  A warp's 32 lanes own 32 consecutive k2
+// columns: G4 rows are read/written as contiguous 512 B runs, staged rows as
+// contiguous (forward or reversed) runs.  The G4 block is read once, receives
+// every walker of the batch in order (bitwise identical to sequential
+// reference calls), and is written once: HBM traffic per pass is
 // 2 * P * N^2 * 16 B plus the staged payloads.
 //
 // v1 (k_accumulate): CTA = WARPS warps stacked along K3 (they share the direct
 //    elements and most shifted rows through L1); loads straight from global.
-// v2 (k_accumulate_tma, complex128 and complex64, N >= 64): one producer lane (lane 0 of
-//    warp 0, which is also a consumer) streams, per walker, two TMA tensor boxes
-//    into a 3-stage shared-memory ring (3 CTAs per SM): the CTA's direct tile (4 rows x 35 cols x 2 spins) through a plain
-//    tensor map, and its whole shifted band (19 diagonal row segments x 32
-//    cols x 2 spins) through a *sheared* tensor map (row stride LD+1 elements)
-//    that turns the diagonal band into a rectangular box.  The halo of the
-//    staged layout means no box ever wraps.  Consumers (4 warps, planes
-//    q0..q0+15) wait on the stage's mbarrier, read their elements from shared
-//    memory (contiguous per warp: conflict-free) and release the stage.
+// v2 (k_accumulate_tma, N >= 64 and >= 4 planes): CTA = CWQ x CWR warps (tile Q
+//    planes x DR diagonal entries x 32 columns, see V2Geom).  One producer lane
+//    (lane 0 of warp 0, which is also a consumer) streams, per walker, two TMA
+//    tensor boxes into an NST-stage shared-memory ring: the CTA's direct tile
+//    (DR rows x 32 cols x 2 spins) and its whole shifted band (Q+DR-1 diagonal
+//    row segments x 32 cols x 2 spins), both through *sheared* tensor maps (row
+//    stride LD+1 elements) that turn diagonals into rectangular boxes.  The halo
+//    of the staged layout means no box ever wraps.  Consumers wait on the
+//    stage's mbarrier, read their elements from shared memory (contiguous per
+//    warp: conflict-free) and release the stage.  Geometry choice and the
+//    measured alternatives: launch_v2_geom below, DESIGN.md section 4.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
