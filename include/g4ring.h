@@ -213,6 +213,50 @@ g4_status g4_round_program_run(void* prog, int64_t m, int32_t regenerate);
 g4_status g4_round_program_k1_ms(void* prog, double* mean_ms, int32_t* count);
 g4_status g4_round_program_destroy(void* prog);
 
+/* ---- native ring driver (replaces ringacc/engine.py:119-161 run_measurement,
+ * the slice assignment and sub-ring split of engine.py:241-255, and the final
+ * reduce of engine.py:251,267 / transport/base.py:126-149) for hosts without
+ * Python.  One ring object per rank (process or thread), one GPU per rank
+ * (the caller selects the device before g4_ring_create).  The host supplies
+ * the control plane as an all-gather callback: gather `bytes` bytes from every
+ * member of `group` into recv (member order: sub-ring position for
+ * G4_GROUP_SUBRING, sub-ring index for G4_GROUP_POSITION); return 0 on success.
+ * The data path (payload copies, flags, K1/K3) never returns to the host. */
+typedef enum { G4_GROUP_SUBRING = 0, G4_GROUP_POSITION = 1 } g4_group;
+typedef int32_t (*g4_allgather_fn)(void* ctx, int32_t group, const void* send, int64_t bytes, void* recv);
+typedef struct {
+    int32_t n_k, n_w;       /* CombinedIndexSpace (tensor.py:31-47) */
+    int32_t world_size;     /* ranks */
+    int32_t subring_size;   /* S, divides world_size (engine.py:86-92) */
+    int32_t lanes;          /* walker streams per rank (< 1000) */
+    int32_t alternate;      /* 0: all lanes forward; 1: odd lanes run backward */
+    int32_t batch;          /* measurements per lane per round (B); B * lanes <= G4_MAX_BATCH */
+    int32_t dtype;          /* G4_C128, G4_C64 or G4_C128_G64 */
+    int64_t planes;         /* exchange planes K3 in [0, planes); 0 = all N */
+    int32_t value_mode;     /* G4_MODE_FLOAT / G4_MODE_INTEGER (synthetic walkers) */
+    int32_t reserved;
+    uint64_t seed;
+} g4_ring_config;
+g4_status g4_ring_create(const g4_ring_config* cfg, int32_t world_rank, g4_allgather_fn allgather, void* ctx,
+                         void** ring);
+/* Enqueue measurement round m (rounds are consecutive from 0): K3-generated
+ * walkers (regenerate != 0) or the payloads already in GEN (g4_ring_stage). */
+g4_status g4_ring_measure(void* ring, int64_t m, int32_t regenerate);
+/* Stage host-fed reference-layout walkers (device pointers) into GEN: count =
+ * batch x lanes, channel order, batch-major (engine.RingEngine.stage_gen). */
+g4_status g4_ring_stage(void* ring, const void* const* up, const void* const* down, int32_t count,
+                        int32_t dtype_in);
+/* Host watchdog: all of this rank's streams drained within timeout_ms, else
+ * G4_ERR_DEADLOCK naming (rank, lane, measurement, step) (inprocess.py:54-60). */
+g4_status g4_ring_wait(void* ring, int64_t timeout_ms);
+/* This rank's G4 slice (device memory, reference layout [k3-lo][k1][k2]). */
+g4_status g4_ring_slice(void* ring, void** data, int64_t* lo, int64_t* hi);
+/* Sum the slices of every sub-ring into sub-ring 0's, in sub-ring order
+ * (collective over the position group). */
+g4_status g4_ring_reduce(void* ring);
+/* Collective over the sub-ring: drain, then free. */
+g4_status g4_ring_destroy(void* ring);
+
 #ifdef __cplusplus
 }
 #endif

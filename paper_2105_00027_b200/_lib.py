@@ -59,7 +59,26 @@ SIGNATURES = {
     "g4_round_program_run": (_i32, [_vp, _i64, _i32]),
     "g4_round_program_k1_ms": (_i32, [_vp, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(_i32)]),
     "g4_round_program_destroy": (_i32, [_vp]),
+    "g4_ring_create": (_i32, [_vp, _i32, _vp, _vp, _vpp]),
+    "g4_ring_measure": (_i32, [_vp, _i64, _i32]),
+    "g4_ring_stage": (_i32, [_vp, _vpp, _vpp, _i32, _i32]),
+    "g4_ring_wait": (_i32, [_vp, _i64]),
+    "g4_ring_slice": (_i32, [_vp, _vpp, _i64p, _i64p]),
+    "g4_ring_reduce": (_i32, [_vp]),
+    "g4_ring_destroy": (_i32, [_vp]),
 }
+
+G4_GROUP_SUBRING, G4_GROUP_POSITION = 0, 1
+# int32_t (*g4_allgather_fn)(void* ctx, int32_t group, const void* send, int64_t bytes, void* recv)
+ALLGATHER_FN = ctypes.CFUNCTYPE(_i32, _vp, _i32, _vp, _i64, _vp)
+
+
+class RingConfig(ctypes.Structure):
+    """g4_ring_config (include/g4ring.h)."""
+
+    _fields_ = [("n_k", _i32), ("n_w", _i32), ("world_size", _i32), ("subring_size", _i32), ("lanes", _i32),
+                ("alternate", _i32), ("batch", _i32), ("dtype", _i32), ("planes", _i64), ("value_mode", _i32),
+                ("reserved", _i32), ("seed", _u64)]
 
 _lock = threading.Lock()
 _lib = None

@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libg4ring.so"
-SOURCES = ["g4_util.cpp", "g4_accumulate.cu", "g4_prep.cu", "g4_ring.cu"]
+SOURCES = ["g4_util.cpp", "g4_accumulate.cu", "g4_prep.cu", "g4_ring.cu", "g4_ring_driver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
