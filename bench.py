@@ -491,10 +491,31 @@ def run_e2e(args, lib, T, sp, planes, dtype, eb, dev):
     t1.record(comp)
     torch.cuda.synchronize()
     ms = t0.elapsed_time(t1)
+    h2d_bytes = B * 2 * n * n * eb
     return {"value": B * planes * n * n * steps / (ms * 1e-3), "unit": "updates/s",
-            "h2d_bytes_per_step": B * 2 * n * n * eb, "d2h_bytes_per_step": n * eb,
+            "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": n * eb,
+            "h2d_gbs_achieved": h2d_bytes * steps / (ms * 1e-3) / 1e9,
+            "h2d_peak_gbs": pinned_h2d_peak(dev),
             "path": "g4_accumulate (C ABI, reference layout) from pinned host buffers; "
                     "H2D double-buffered on a copy stream; D2H probe row per step"}
+
+
+def pinned_h2d_peak(dev, nbytes=256 << 20, reps=5):
+    """Measured pinned host -> device copy bandwidth (GB/s): the ceiling of
+    the e2e leg, whose per-step H2D of the walkers' reference-layout G's is
+    its bound."""
+    import torch
+    src = torch.empty(nbytes, dtype=torch.uint8).pin_memory()
+    dst = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    dst.copy_(src, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record()
+    for _ in range(reps):
+        dst.copy_(src, non_blocking=True)
+    b.record()
+    torch.cuda.synchronize(dev)
+    return nbytes * reps / (a.elapsed_time(b) * 1e-3) / 1e9
 
 
 def _dtype_code(dtype):
