@@ -593,7 +593,7 @@ def run_ring(args):
     peb = 16 if args.dtype == "c128" else 8
     alg_bytes = 2 * p_local * n * n * eb + B * lanes * 2 * n * n * peb
     achieved = alg_bytes / (kms * 1e-3) / 1e9
-    ring_bytes = (S - 1) * B * lanes * eng.payload_bytes
+    ring_bytes = (S - 1) * B * lanes * eng.wire_bytes
     line = {
         "metric": "G4 updates/s", "value": value, "unit": "updates/s", "n_gpus": n_ranks,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,

@@ -169,6 +169,13 @@ g4_status g4_ipc_close(void* dev_ptr);
 
 /* Stream-ordered peer copy (copy engine over NVLink/NVSwitch, or local). */
 g4_status g4_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* The N x N cores (both spins) of `count` consecutive staged payloads, as one
+ * strided peer copy: the ring's wire format.  The halo is not sent. */
+g4_status g4_copy_payload_cores(void* dst, const void* src, int32_t count, int32_t n, int32_t dtype,
+                                void* stream);
+/* Rebuild the cyclic halo of staged payloads from their cores (the receiver
+ * side of g4_copy_payload_cores). */
+g4_status g4_fill_halo(void* const* staged, int32_t count, int32_t n, int32_t dtype, void* stream);
 
 /* Stream-ordered 64-bit flag write / wait (cuStreamWriteValue64 /
  * cuStreamWaitValue64 with GEQ).  `flag` may be a peer (IPC-mapped) address. */
@@ -194,7 +201,10 @@ g4_status g4_reduce_sum(void* dst, const void* const* src, int32_t nsrc, int64_t
  *   {G4_OP_ACC,   stream, ptr_off, count}        K1 on ptrs[ptr_off .. +count)
  *   {G4_OP_WAIT,  stream, flag, base, slope}     wait flag >= base + slope*m
  *   {G4_OP_WRITE, stream, flag, base, slope}     write base + slope*m
- *   {G4_OP_COPY,  stream, dst, src, nbytes}      peer copy
+ *   {G4_OP_COPY,  stream, dst, src, nbytes, count, n, dtype}
+ *                                                peer copy: `nbytes` bytes, or (count > 0)
+ *                                                the cores of `count` staged payloads
+ *   {G4_OP_HALO,  stream, ptr_off, count}        g4_fill_halo on ptrs[ptr_off .. +count)
  *   {G4_OP_RECORD / G4_OP_WAIT_EVENT, stream, event}
  *   {G4_OP_GEN,   stream, ptr_off, count, meta_off}  K3 into ptrs with
  *       meta[meta_off ..] = world_rank[count], lane[count], meas_base[count];
@@ -202,7 +212,7 @@ g4_status g4_reduce_sum(void* dst, const void* const* src, int32_t nsrc, int64_t
  * streams, events and ptrs are borrowed for the program's lifetime. */
 #define G4_OP_WORDS 8
 enum { G4_OP_ACC = 1, G4_OP_WAIT = 2, G4_OP_WRITE = 3, G4_OP_COPY = 4, G4_OP_RECORD = 5,
-       G4_OP_WAIT_EVENT = 6, G4_OP_GEN = 7 };
+       G4_OP_WAIT_EVENT = 6, G4_OP_GEN = 7, G4_OP_HALO = 8 };
 g4_status g4_round_program_create(const int64_t* ops, int32_t nops, void* const* ptrs, int32_t nptrs,
                                   const int64_t* meta, int32_t nmeta, void* const* streams, int32_t nstreams,
                                   void* const* events, int32_t nevents, void* g4, int64_t lo, int64_t hi, int32_t n, int32_t dtype,

@@ -24,7 +24,7 @@ G4_MAX_BATCH = 64
 G4_IPC_HANDLE_BYTES = 64
 G4_HALO_ROWS, G4_HALO_COLS = 40, 72
 G4_OP_WORDS = 8
-G4_OP_ACC, G4_OP_WAIT, G4_OP_WRITE, G4_OP_COPY, G4_OP_RECORD, G4_OP_WAIT_EVENT, G4_OP_GEN = range(1, 8)
+G4_OP_ACC, G4_OP_WAIT, G4_OP_WRITE, G4_OP_COPY, G4_OP_RECORD, G4_OP_WAIT_EVENT, G4_OP_GEN, G4_OP_HALO = range(1, 9)
 ABI_VERSION = 1
 
 # (name, restype, argtypes) for every symbol include/g4ring.h declares.
@@ -50,6 +50,8 @@ SIGNATURES = {
     "g4_ipc_import": (_i32, [_vp, _i64, _vpp]),
     "g4_ipc_close": (_i32, [_vp]),
     "g4_copy_async": (_i32, [_vp, _vp, _i64, _vp]),
+    "g4_copy_payload_cores": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp]),
+    "g4_fill_halo": (_i32, [_vpp, _i32, _i32, _i32, _vp]),
     "g4_flag_write": (_i32, [_vp, _u64, _vp]),
     "g4_flag_wait": (_i32, [_vp, _u64, _vp]),
     "g4_flag_host_wait": (_i32, [_vp, _u64, _i64]),

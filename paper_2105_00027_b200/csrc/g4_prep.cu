@@ -89,6 +89,61 @@ static g4_status prepare_t(void* const* staged, const void* const* up, const voi
 }
 
 // ---------------------------------------------------------------------------
+// Halo rebuild: stg[s][r][c] = stg[s][r mod N][c mod N] for every entry
+// outside the N x N core (rows >= N or columns >= N).  The ring moves only
+// payload cores (g4_copy_payload_cores); each receiver restores the halo its
+// TMA boxes need.  blockIdx.y = walker * 2 + spin; a flat grid-stride index
+// over the bottom band (rows N..ROWS-1, all columns) then the right band
+// (rows 0..N-1, columns N..LD-1).
+template <typename R>
+struct HaloParams {
+    Cx<R>* stg[MAXB];
+    int32_t n;
+};
+
+template <typename R>
+__global__ void __launch_bounds__(256) k_fill_halo(const __grid_constant__ HaloParams<R> P) {
+    const int n = P.n;
+    const int ld = staged_ld(n, sizeof(Cx<R>)), rows = staged_rows(n, sizeof(Cx<R>));
+    const int w = blockIdx.y >> 1, s = blockIdx.y & 1;
+    Cx<R>* base = P.stg[w] + (int64_t)s * staged_plane(n, sizeof(Cx<R>));
+    const int64_t bottom = (int64_t)(rows - n) * ld, right = (int64_t)n * (ld - n);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < bottom + right;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int r, c;
+        if (i < bottom) {
+            r = n + (int)(i / ld);
+            c = (int)(i % ld);
+        } else {
+            const int64_t j = i - bottom;
+            r = (int)(j / (ld - n));
+            c = n + (int)(j % (ld - n));
+        }
+        base[(int64_t)r * ld + c] = base[(int64_t)(r % n) * ld + (c % n)];
+    }
+}
+
+template <typename R>
+static g4_status fill_halo_t(void* const* staged, int32_t count, int32_t n, cudaStream_t st) {
+    for (int32_t b0 = 0; b0 < count; b0 += MAXB) {
+        HaloParams<R> prm{};
+        const int nb = std::min<int32_t>(MAXB, count - b0);
+        for (int i = 0; i < nb; ++i) {
+            if (!staged[b0 + i] || !aligned(staged[b0 + i], sizeof(Cx<R>)))
+                return fail(G4_ERR_CONTRACT, "fill_halo: null or misaligned payload");
+            prm.stg[i] = static_cast<Cx<R>*>(staged[b0 + i]);
+        }
+        prm.n = n;
+        const int64_t halo = (int64_t)(staged_rows(n, sizeof(Cx<R>)) - n) * staged_ld(n, sizeof(Cx<R>)) +
+                             (int64_t)n * (staged_ld(n, sizeof(Cx<R>)) - n);
+        const unsigned bx = (unsigned)std::min<int64_t>((halo + 255) / 256, 1024);
+        k_fill_halo<R><<<dim3(bx, 2 * nb), 256, 0, st>>>(prm);
+        G4_CUDA(cudaGetLastError());
+    }
+    return G4_OK;
+}
+
+// ---------------------------------------------------------------------------
 // K3: generator.  Entry idx of matrix m of walker (seed, world_rank, lane, meas):
 //   key  = stream_key(seed, world_rank, lane, meas, m)            (tensor.py:182-186)
 //   u1   = top53(mix(key ^ 2 idx)),  u2 = top53(mix(key ^ (2 idx + 1)))  (tensor.py:196-198)
@@ -235,6 +290,17 @@ g4_status g4_prepare_g(void* const* staged, const void* const* up, const void* c
     if (dtype_in == G4_C128 && dtype_out == G4_C64)
         return prepare_t<double, float>(staged, up, down, nbatch, n, st);
     return fail(G4_ERR_CONTRACT, "prepare_g: unsupported dtype pair");
+}
+
+g4_status g4_fill_halo(void* const* staged, int32_t count, int32_t n, int32_t dtype, void* stream) {
+    using namespace g4;
+    if (n < 1 || count < 0) return fail(G4_ERR_CONTRACT, "fill_halo: bad n or count");
+    if (count == 0) return G4_OK;
+    if (!staged) return fail(G4_ERR_CONTRACT, "fill_halo: null pointer list");
+    auto st = static_cast<cudaStream_t>(stream);
+    if (dtype == G4_C128) return fill_halo_t<double>(staged, count, n, st);
+    if (dtype == G4_C64) return fill_halo_t<float>(staged, count, n, st);
+    return fail(G4_ERR_CONTRACT, "fill_halo: unknown dtype");
 }
 
 g4_status g4_generate(void* const* staged, void* const* up, void* const* down, int32_t nbatch,

@@ -146,6 +146,26 @@ g4_status g4_copy_async(void* dst, const void* src, int64_t bytes, void* stream)
     return G4_OK;
 }
 
+// The N x N cores of `count` consecutive staged payloads (both spins), as one
+// strided copy-engine transfer: the halo (23 % of a payload at N = 512) never
+// crosses NVLink; the receiver rebuilds it (g4_fill_halo).
+g4_status g4_copy_payload_cores(void* dst, const void* src, int32_t count, int32_t n, int32_t dtype,
+                                void* stream) {
+    using namespace g4;
+    if (!dst || !src || count < 0 || n < 1 || (dtype != G4_C128 && dtype != G4_C64))
+        return fail(G4_ERR_CONTRACT, "copy_payload_cores: bad args");
+    if (count == 0) return G4_OK;
+    const size_t eb = entry_bytes(dtype);
+    const size_t pitch = (size_t)staged_ld(n, (int)eb) * eb, rows = (size_t)staged_rows(n, (int)eb);
+    cudaMemcpy3DParms p{};
+    p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), pitch, (size_t)n * eb, rows);
+    p.dstPtr = make_cudaPitchedPtr(dst, pitch, (size_t)n * eb, rows);
+    p.extent = make_cudaExtent((size_t)n * eb, (size_t)n, (size_t)2 * count);  // [walker, spin] planes
+    p.kind = cudaMemcpyDeviceToDevice;
+    G4_CUDA(cudaMemcpy3DAsync(&p, static_cast<cudaStream_t>(stream)));
+    return G4_OK;
+}
+
 g4_status g4_flag_write(void* flag, uint64_t value, void* stream) {
     using namespace g4;
     static PFN_write64 fn = nullptr;
@@ -288,10 +308,11 @@ g4_status g4_round_program_create(const int64_t* ops, int32_t nops, void* const*
         const int64_t* o = &P->ops[(size_t)i * G4_OP_WORDS];
         const int64_t kind = o[0], st = o[1];
         bool ok = st >= 0 && st < nstreams;
-        if (kind == G4_OP_ACC || kind == G4_OP_GEN) ok = ok && o[2] >= 0 && o[3] >= 1 && o[2] + o[3] <= nptrs;
+        if (kind == G4_OP_ACC || kind == G4_OP_GEN || kind == G4_OP_HALO)
+            ok = ok && o[2] >= 0 && o[3] >= 1 && o[2] + o[3] <= nptrs;
         if (kind == G4_OP_GEN) ok = ok && o[4] >= 0 && o[4] + 3 * o[3] <= nmeta;
         if (kind == G4_OP_RECORD || kind == G4_OP_WAIT_EVENT) ok = ok && o[2] >= 0 && o[2] < nevents;
-        if (kind < G4_OP_ACC || kind > G4_OP_GEN) ok = false;
+        if (kind < G4_OP_ACC || kind > G4_OP_HALO) ok = false;
         if (!ok) {
             delete P;
             set_error("round_program_create: malformed op %d (kind %lld)", i, (long long)kind);
@@ -355,7 +376,14 @@ g4_status g4_round_program_run(void* prog, int64_t m, int32_t regenerate) {
                 G4_TRY(g4_flag_write(reinterpret_cast<void*>(o[2]), (uint64_t)(o[3] + o[4] * m), st));
                 break;
             case G4_OP_COPY:
-                G4_TRY(g4_copy_async(reinterpret_cast<void*>(o[2]), reinterpret_cast<const void*>(o[3]), o[4], st));
+                if (o[5] > 0)  // payload cores: count o[5], N o[6], dtype o[7]
+                    G4_TRY(g4_copy_payload_cores(reinterpret_cast<void*>(o[2]), reinterpret_cast<const void*>(o[3]),
+                                                 (int32_t)o[5], (int32_t)o[6], (int32_t)o[7], st));
+                else
+                    G4_TRY(g4_copy_async(reinterpret_cast<void*>(o[2]), reinterpret_cast<const void*>(o[3]), o[4], st));
+                break;
+            case G4_OP_HALO:
+                G4_TRY(g4_fill_halo(&P->ptrs[o[2]], (int32_t)o[3], P->n, P->pdtype, st));
                 break;
             case G4_OP_RECORD:
                 G4_CUDA(cudaEventRecord(P->events[o[2]], st));

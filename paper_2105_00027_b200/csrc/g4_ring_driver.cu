@@ -8,8 +8,9 @@
 // package): per channel (lanes sharing a direction) three staged payload
 // buffers GEN, R0, R1 and three 64-bit flags DATA, ACK_ACC, ACK_FWD; round m,
 // step j moves transfer k = 2 + m(S-1) + j into slot k % 2 of the right
-// neighbour with a copy-engine peer copy, announced by a stream flag write;
-// K1 runs on the compute stream once DATA >= k.  The host supplies the control
+// neighbour with a copy-engine peer copy of the payload cores, announced by a
+// stream flag write; the receiver rebuilds the halo and runs K1 on the compute
+// stream once DATA >= k.  The host supplies the control
 // plane as an all-gather callback (rendezvous of IPC handles, barriers); the
 // data path never returns to the host.  Ranks of the same process (threads)
 // share pointers directly; other processes are reached through CUDA IPC.
@@ -330,7 +331,7 @@ g4_status g4_ring_measure(void* ring, int64_t m, int32_t regenerate) {
                 src = R0_BUF + (int)((k - 1) % 2);
             }
             char* dst = reinterpret_cast<char*>(R->peer_bufs[c.index]) + (R0_BUF + k % 2) * R->slot_bytes(c);
-            G4_TRY(g4_copy_async(dst, R->buf(c, src), R->slot_bytes(c), cs));
+            G4_TRY(g4_copy_payload_cores(dst, R->buf(c, src), B * (int32_t)c.lanes.size(), R->n, R->pcode, cs));
             G4_TRY(g4_flag_write(flag(c.send_to, c.index, F_DATA), (uint64_t)k, cs));
             if (j == 0) G4_CUDA(cudaEventRecord(R->ev_sent[c.index], cs));
             if (j >= 1) G4_TRY(g4_flag_write(flag(c.recv_from, c.index, F_ACK_FWD), (uint64_t)(k - 1), cs));
@@ -339,6 +340,9 @@ g4_status g4_ring_measure(void* ring, int64_t m, int32_t regenerate) {
         for (const Chan& c : R->chans) G4_TRY(g4_flag_wait(own_flag(c.index, F_DATA), (uint64_t)k, R->compute));
         ptrs.clear();
         for (const Chan& c : R->chans) add_slot(c, R0_BUF + (int)(k % 2));
+        std::vector<void*> halo(ptrs.size());  // only the cores crossed the link
+        for (size_t i = 0; i < ptrs.size(); ++i) halo[i] = const_cast<void*>(ptrs[i]);
+        G4_TRY(g4_fill_halo(halo.data(), (int32_t)halo.size(), R->n, R->pcode, R->compute));
         G4_TRY(k1(ptrs));
         for (const Chan& c : R->chans)
             G4_TRY(g4_flag_write(flag(c.recv_from, c.index, F_ACK_ACC), (uint64_t)k, R->compute));

@@ -5,7 +5,7 @@ One process per GPU.  ``torch.distributed`` (gloo) is the control plane only:
 rendezvous, communicator splits, the one-time exchange of CUDA IPC handles,
 barriers.  The data path never touches the host:
 
-* payload transfers are copy-engine peer copies (``g4_copy_async``) straight
+* payload transfers are copy-engine peer copies of the payload cores (``g4_copy_payload_cores``) straight
   into the right neighbour's receive slot over NVLink/NVSwitch (no SM cycles);
 * ordering is carried by 64-bit sequence flags in the receiver's / sender's
   memory, written with ``cuStreamWriteValue64`` and awaited with
@@ -262,6 +262,7 @@ class RingEngine:
         self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n, self.pdtype), dtype=self.pdtype,
                                  device=device) for c in self.channels]
         self.payload_bytes = int(np.prod(staged_shape(n, self.pdtype))) * self.bufs[0].element_size()
+        self.wire_bytes = 2 * n * n * self.bufs[0].element_size()  # the cores that cross the link
         self.flags = torch.zeros(len(self.channels) * S.FLAGS_PER_CHANNEL, dtype=torch.int64, device=device)
         self.compute = torch.cuda.Stream(device)
         self.comm = [torch.cuda.Stream(device) for _ in self.channels]
@@ -389,13 +390,19 @@ class RingEngine:
             elif kind == "copy":
                 _, st, ci, src, peer, dst = op
                 c = self.channels[ci]
-                nbytes = nb * len(c.lanes) * self.payload_bytes
+                cnt = nb * len(c.lanes)
                 dst_ptr = self.peer_bufs[(peer, ci)] + dst * self.bufs[ci][0].numel() * self.bufs[ci].element_size()
-                words.append([_lib.G4_OP_COPY, sidx(st), dst_ptr, self._buf_ptr(ci, src), nbytes, 0, 0, 0])
+                words.append([_lib.G4_OP_COPY, sidx(st), dst_ptr, self._buf_ptr(ci, src), 0, cnt,
+                              self.space.size, self.pcode])
                 for t in c.lanes:
                     delta["sent"][t] += nb
                     delta["msgs"][t] += 1
-                    delta["bytes"][t] += nbytes // len(c.lanes)
+                    delta["bytes"][t] += nb * self.wire_bytes
+            elif kind == "halo":
+                off = len(ptrs)
+                for ci, buf in op[1]:
+                    ptrs += [self._buf_ptr(ci, buf, j) for j in range(nb * len(self.channels[ci].lanes))]
+                words.append([_lib.G4_OP_HALO, 0, off, len(ptrs) - off, 0, 0, 0, 0])
             elif kind in ("record", "wait_event"):
                 words.append([_lib.G4_OP_RECORD if kind == "record" else _lib.G4_OP_WAIT_EVENT,
                               sidx(op[1]), ev_names.index(op[2]), 0, 0, 0, 0, 0])
@@ -526,14 +533,19 @@ class RingEngine:
             elif kind == "copy":
                 _, st, ci, src, peer, dst = op
                 c = self.channels[ci]
-                nbytes = nb * len(c.lanes) * self.payload_bytes
+                cnt = nb * len(c.lanes)
                 dst_ptr = self.peer_bufs[(peer, ci)] + dst * self.bufs[ci][0].numel() * self.bufs[ci].element_size()
-                _lib.check(lib.g4_copy_async(dst_ptr, self._buf_ptr(ci, src), nbytes,
-                                             self._stream(st).cuda_stream), "copy_async")
+                _lib.check(lib.g4_copy_payload_cores(dst_ptr, self._buf_ptr(ci, src), cnt, self.space.size,
+                                                     self.pcode, self._stream(st).cuda_stream), "copy_cores")
                 for t in c.lanes:
                     self.counters[t].envelopes_sent += nb
                     self.counters[t].messages_sent += 1
-                    self.counters[t].bytes_sent += nbytes // len(c.lanes)
+                    self.counters[t].bytes_sent += nb * self.wire_bytes
+            elif kind == "halo":
+                ptrs = [self._buf_ptr(ci, buf, i) for ci, buf in op[1]
+                        for i in range(nb * len(self.channels[ci].lanes))]
+                _lib.check(lib.g4_fill_halo(_lib.ptr_array(ptrs), len(ptrs), self.space.size, self.pcode,
+                                            self.compute.cuda_stream), "fill_halo")
             elif kind == "record":
                 self.events[op[2]].record(self._stream(op[1]))
             elif kind == "wait_event":

@@ -193,6 +193,11 @@ def staged_payload_bytes(n: int, dtype: str) -> int:
     return int(_lib.load().g4_payload_bytes(n, code))
 
 
+def wire_payload_bytes(n: int, dtype: str) -> int:
+    """Bytes of one walker on the ring: the N x N cores of both spins (g4_copy_payload_cores)."""
+    return 2 * n * n * payload_entry_bytes(dtype)
+
+
 def device_plan(n: int, planes_total: int, gpus: int, lanes: int = 1, batch: int = 1,
                 dtype: str = "c128", hbm_bytes: float = B200_HBM_BYTES) -> dict:
     """Per-GPU allocation of the ring engine: the G4 slice plus, per channel,
@@ -296,7 +301,10 @@ def ring_round_time(gpus: int, batch: int, n: int, planes_total: int, dtype: str
     p = -(-planes_total // s)
     walkers = batch * lanes
     k1 = k1_pass_time(n, p, walkers, dtype, arith, cal)
-    msg = walkers * staged_payload_bytes(n, dtype)
+    # only the N x N cores cross the link; the receiver rebuilds the halo (HBM read + write)
+    msg = walkers * wire_payload_bytes(n, dtype)
+    halo_s = walkers * 2 * (staged_payload_bytes(n, dtype) - wire_payload_bytes(n, dtype)) / (cal.hbm_gbs * 1e9)
+    k1 = dict(k1, time_s=k1["time_s"] + (halo_s if s > 1 else 0.0))
     _, load, bw = slow_link(s, link, 1)
     xfer = link.latency + msg * load / bw if s > 1 else 0.0
     step = max(k1["time_s"], xfer)
@@ -313,7 +321,7 @@ def hide_planes(n: int, batch: int, dtype: str = "c128", lanes: int = 1, arith: 
                 link: LinkConfig = NVSWITCH_B200, cal: K1Calibration = B200_K1, max_planes: int = 4096) -> int:
     """Smallest per-GPU slice (planes) whose K1 pass hides one ring step
     (0 if none up to ``max_planes``)."""
-    msg = batch * lanes * staged_payload_bytes(n, dtype)
+    msg = batch * lanes * wire_payload_bytes(n, dtype)
     xfer = link.latency + msg / link.intra_bandwidth
     lo, hi = 1, max_planes
     if k1_pass_time(n, hi, batch * lanes, dtype, arith, cal)["time_s"] < xfer:

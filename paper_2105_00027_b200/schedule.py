@@ -24,6 +24,8 @@ B200 realisation (one round = B measurements of every lane):
   * transfer k (k = 2 + m*(S-1) + j for round m, step j) lands in slot k % 2 of
     the receiver; before sending it the sender waits until the receiver has
     both accumulated and forwarded transfer k - 2 (which occupied that slot).
+  * only the N x N payload cores cross the link; the receiver rebuilds the
+    staged layout's halo on its compute stream before K1 reads the slot.
 """
 from __future__ import annotations
 
@@ -131,7 +133,8 @@ def birth_position(pos: int, j: int, s: int, backward: bool) -> int:
 #   ("acc", ((channel, buf), ...), tag)          compute: one K1 pass over those buffers
 #   ("wait", stream, channel, flag, value)       stream blocks until my flag >= value
 #   ("write", stream, peer_pos, channel, flag, value)  stream writes the flag on a neighbour
-#   ("copy", stream, channel, src_buf, peer_pos, dst_buf)  copy-engine transfer
+#   ("copy", stream, channel, src_buf, peer_pos, dst_buf)  copy-engine transfer of the payload cores
+#   ("halo", ((channel, buf), ...))              compute: rebuild the halo of received payloads
 #   ("record", stream, event) / ("wait_event", stream, event)
 
 
@@ -176,6 +179,7 @@ def round_schedule(topo: RingTopology, pos: int, channels: list[Channel], m: int
                 ops.append(("write", cs, c.recv_from, c.index, ACK_FWD, k))
         for c in channels:
             ops.append(("wait", COMPUTE, c.index, DATA, k))
+        ops.append(("halo", tuple((c.index, R0 + k % 2) for c in channels)))
         ops.append(("acc", tuple((c.index, R0 + k % 2) for c in channels), ("ring", m, j)))
         for c in channels:
             ops.append(("write", COMPUTE, c.recv_from, c.index, ACK_ACC, k))

@@ -71,7 +71,7 @@ def run_subring(topo, subring, n, lo_hi, seed, rounds, batch, mode="integer", st
                 bound.append(op)
         streams = {}
         for op in bound:
-            streams.setdefault(S.COMPUTE if op[0] in ("gen", "acc") else op[1], []).append(op)
+            streams.setdefault(S.COMPUTE if op[0] in ("gen", "acc", "halo") else op[1], []).append(op)
         for name, lst in streams.items():
             th = threading.Thread(target=_stream_main, args=(ranks, st, lst, seed, mode, timeout, errors),
                                   daemon=True)
@@ -139,6 +139,8 @@ def _execute(ranks, st, op, seed, mode, timeout):
         tgt.bufs[(ci_peer(tgt, st, ci), dst)] = payloads
         for p in payloads:  # payloads (measurements) sent, per lane
             st.sent[p["origin"][2]] += 1
+    elif kind == "halo":
+        pass  # the simulator's payloads carry no halo
     elif kind == "record":
         with st.ev_cv:
             st.events[op[2]] = op[3]

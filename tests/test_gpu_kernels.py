@@ -352,3 +352,25 @@ def test_mixed_precision_bitwise(oracle, cuda_dev, n, lo, hi, variant):
         assert np.array_equal(to_np(sl.data), ref)
     finally:
         _lib.check(lib.g4_set_kernel_variant(0))
+
+
+@pytest.mark.parametrize("n,dtype", [(32, torch.complex128), (100, torch.complex128), (512, torch.complex128),
+                                     (96, torch.complex64), (257, torch.complex64)])
+def test_core_copy_plus_halo_rebuild_is_exact(cuda_dev, n, dtype):
+    """The ring's wire format: g4_copy_payload_cores moves only the N x N cores
+    of staged payloads, g4_fill_halo rebuilds the rest; together they give the
+    staged payloads bit for bit."""
+    lib = _lib.load()
+    sp = T.CombinedIndexSpace(1, n)
+    code = _lib.G4_C128 if dtype == torch.complex128 else _lib.G4_C64
+    k = 3
+    src = torch.empty((k,) + T.staged_shape(n, dtype), dtype=dtype, device=cuda_dev)
+    for i in range(k):
+        g = T.generate_gsigma(i, T.Origin(0, 0, i, 0, 0), sp, "float", device=cuda_dev, dtype=dtype)
+        src[i].copy_(g.staged)
+    dst = torch.full_like(src, complex(float("nan"), float("nan")))
+    st = torch.cuda.current_stream(cuda_dev).cuda_stream
+    _lib.check(lib.g4_copy_payload_cores(dst.data_ptr(), src.data_ptr(), k, n, code, st))
+    _lib.check(lib.g4_fill_halo(_lib.ptr_array([dst[i].data_ptr() for i in range(k)]), k, n, code, st))
+    torch.cuda.synchronize()
+    assert torch.equal(torch.view_as_real(dst), torch.view_as_real(src))
