@@ -176,6 +176,11 @@ g4_status g4_copy_payload_cores(void* dst, const void* src, int32_t count, int32
 /* Rebuild the cyclic halo of staged payloads from their cores (the receiver
  * side of g4_copy_payload_cores). */
 g4_status g4_fill_halo(void* const* staged, int32_t count, int32_t n, int32_t dtype, void* stream);
+/* Load the kernels a ring launches behind stream flag waits (CUDA loads
+ * kernels lazily at first launch, and a load cannot complete while the
+ * context has a blocked stream).  Ring hosts call it once before their first
+ * round; g4_ring_create does. */
+g4_status g4_preload_ring_kernels(void);
 
 /* Stream-ordered 64-bit flag write / wait (cuStreamWriteValue64 /
  * cuStreamWaitValue64 with GEQ).  `flag` may be a peer (IPC-mapped) address. */

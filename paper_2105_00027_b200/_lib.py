@@ -52,6 +52,7 @@ SIGNATURES = {
     "g4_copy_async": (_i32, [_vp, _vp, _i64, _vp]),
     "g4_copy_payload_cores": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp]),
     "g4_fill_halo": (_i32, [_vpp, _i32, _i32, _i32, _vp]),
+    "g4_preload_ring_kernels": (_i32, []),
     "g4_flag_write": (_i32, [_vp, _u64, _vp]),
     "g4_flag_wait": (_i32, [_vp, _u64, _vp]),
     "g4_flag_host_wait": (_i32, [_vp, _u64, _i64]),

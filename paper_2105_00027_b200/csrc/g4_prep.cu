@@ -292,6 +292,17 @@ g4_status g4_prepare_g(void* const* staged, const void* const* up, const void* c
     return fail(G4_ERR_CONTRACT, "prepare_g: unsupported dtype pair");
 }
 
+// CUDA loads kernels lazily at their first launch, and a load waits for the
+// context.  The halo kernel is first launched behind a ring flag wait, so it
+// is loaded up front by the ring hosts (engine.RingEngine, g4_ring_create).
+g4_status g4_preload_ring_kernels(void) {
+    using namespace g4;
+    cudaFuncAttributes a;
+    G4_CUDA(cudaFuncGetAttributes(&a, k_fill_halo<double>));
+    G4_CUDA(cudaFuncGetAttributes(&a, k_fill_halo<float>));
+    return G4_OK;
+}
+
 g4_status g4_fill_halo(void* const* staged, int32_t count, int32_t n, int32_t dtype, void* stream) {
     using namespace g4;
     if (n < 1 || count < 0) return fail(G4_ERR_CONTRACT, "fill_halo: bad n or count");

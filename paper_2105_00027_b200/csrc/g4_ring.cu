@@ -192,8 +192,7 @@ g4_status g4_flag_wait(const void* flag, uint64_t value, void* stream) {
     if (flush < 0) {
         int dev = 0, v = 0;
         flush = (cudaGetDevice(&dev) == cudaSuccess &&
-                 cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev) == cudaSuccess && v)
-                    ? 1 : 0;
+                 cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev) == cudaSuccess && v) ? 1 : 0;
     }
     const unsigned int how = CU_STREAM_WAIT_VALUE_GEQ | (flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
     CUresult r = fn(static_cast<CUstream>(stream), (CUdeviceptr)flag, (cuuint64_t)value, how);

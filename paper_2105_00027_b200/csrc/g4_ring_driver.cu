@@ -164,6 +164,7 @@ g4_status g4_ring_create(const g4_ring_config* cfg, int32_t world_rank, g4_allga
     if (cfg->value_mode != G4_MODE_FLOAT && cfg->value_mode != G4_MODE_INTEGER)
         return fail(G4_ERR_CONFIG, "unknown value mode");
 
+    G4_TRY(g4_preload_ring_kernels());
     auto* R = new Ring();
     R->cfg = *cfg;
     R->cfg.planes = planes;

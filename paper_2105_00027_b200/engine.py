@@ -258,6 +258,7 @@ class RingEngine:
         self.slice = GtSlice.zeros(self.space, self.lo, self.hi, device=device, dtype=self.dtype)
         self.channels = S.make_channels(self.topo, self.pos)
         self.lib = _lib.load()
+        _lib.check(self.lib.g4_preload_ring_kernels(), "preload_ring_kernels")
         # per channel: 3 buffers (GEN, R0, R1) x batch x lanes staged payloads
         self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n, self.pdtype), dtype=self.pdtype,
                                  device=device) for c in self.channels]
