@@ -157,12 +157,29 @@ g4_status g4_copy_payload_cores(void* dst, const void* src, int32_t count, int32
     if (count == 0) return G4_OK;
     const size_t eb = entry_bytes(dtype);
     const size_t pitch = (size_t)staged_ld(n, (int)eb) * eb, rows = (size_t)staged_rows(n, (int)eb);
-    cudaMemcpy3DParms p{};
-    p.srcPtr = make_cudaPitchedPtr(const_cast<void*>(src), pitch, (size_t)n * eb, rows);
-    p.dstPtr = make_cudaPitchedPtr(dst, pitch, (size_t)n * eb, rows);
-    p.extent = make_cudaExtent((size_t)n * eb, (size_t)n, (size_t)2 * count);  // [walker, spin] planes
-    p.kind = cudaMemcpyDeviceToDevice;
-    G4_CUDA(cudaMemcpy3DAsync(&p, static_cast<cudaStream_t>(stream)));
+    const cudaPitchedPtr sp = make_cudaPitchedPtr(const_cast<void*>(src), pitch, (size_t)n * eb, rows);
+    const cudaPitchedPtr dp = make_cudaPitchedPtr(dst, pitch, (size_t)n * eb, rows);
+    const cudaExtent ext = make_cudaExtent((size_t)n * eb, (size_t)n, (size_t)2 * count);  // [walker, spin] planes
+    // A peer on another GPU (IPC-mapped over NVLink) takes the explicit peer form.
+    cudaPointerAttributes as{}, ad{};
+    G4_CUDA(cudaPointerGetAttributes(&as, src));
+    G4_CUDA(cudaPointerGetAttributes(&ad, dst));
+    if (as.device != ad.device) {
+        cudaMemcpy3DPeerParms p{};
+        p.srcPtr = sp;
+        p.srcDevice = as.device;
+        p.dstPtr = dp;
+        p.dstDevice = ad.device;
+        p.extent = ext;
+        G4_CUDA(cudaMemcpy3DPeerAsync(&p, static_cast<cudaStream_t>(stream)));
+    } else {
+        cudaMemcpy3DParms p{};
+        p.srcPtr = sp;
+        p.dstPtr = dp;
+        p.extent = ext;
+        p.kind = cudaMemcpyDeviceToDevice;
+        G4_CUDA(cudaMemcpy3DAsync(&p, static_cast<cudaStream_t>(stream)));
+    }
     return G4_OK;
 }
 
