@@ -171,7 +171,14 @@ g4_status g4_copy_payload_cores(void* dst, const void* src, int32_t count, int32
         p.dstPtr = dp;
         p.dstDevice = ad.device;
         p.extent = ext;
-        G4_CUDA(cudaMemcpy3DPeerAsync(&p, static_cast<cudaStream_t>(stream)));
+        if (cudaMemcpy3DPeerAsync(&p, static_cast<cudaStream_t>(stream)) != cudaSuccess) {
+            // no strided peer copy here: move whole staged payloads (the halo
+            // rebuild on the receiver is then a no-op rewrite)
+            cudaGetLastError();
+            const int64_t bytes = (int64_t)2 * count * (int64_t)rows * (int64_t)pitch;
+            G4_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                                    static_cast<cudaStream_t>(stream)));
+        }
     } else {
         cudaMemcpy3DParms p{};
         p.srcPtr = sp;
