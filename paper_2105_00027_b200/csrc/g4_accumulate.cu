@@ -280,9 +280,10 @@ constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel 
 // e < DR).  Per walker the CTA fetches DR direct rows and Q + DR - 1 band rows
 // (32 entries x 2 spins each): (Q + 2 DR - 1) / (Q DR) rows per G4 entry.
 // NST-stage shared-memory ring, payload entry type R.
-template <typename R, int PP_, int CW_, int NST_, int DD_ = 4, int CWR_ = 1>
+template <typename R, int PP_, int CW_, int NST_, int DD_ = 4, int CWR_ = 1, int PF_ = 1>
 struct V2Geom {
     static constexpr int PP = PP_, DD = DD_, CWQ = CW_, CWR = CWR_, NST = NST_;
+    static constexpr int PF = PF_;  // shifted operands loaded this many diagonals ahead
     static constexpr int CW = CWQ * CWR;                          // warps per CTA
     static constexpr int Q = PP * CWQ, DR = DD * CWR;             // CTA tile: planes x diagonal entries
     static constexpr int ES = sizeof(Cx<R>);                      // bytes per complex entry
@@ -451,7 +452,12 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         Stg<R> dv[DD];
 #pragma unroll
         for (int d = 0; d < DD; ++d) dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
-        Stg<R> snext = widen<R>(lds_plain(sh_u + sh_o, sh_d + sh_o));
+        constexpr int NJ = PP + DD - 1;  // diagonals
+        constexpr int PF = G::PF < NJ ? G::PF : NJ;
+        Stg<R> sbuf[PF];  // register ring of the next PF diagonals' shifted operands
+#pragma unroll
+        for (int i = 0; i < PF; ++i)
+            sbuf[i] = widen<R>(lds_plain(sh_u + sh_o + i * G::W, sh_d + sh_o + i * G::W));
         // Producer duty (lane 0 of warp 0): refill the stage every warp released in
         // the previous iteration with walker w - 1 + NST; its TMA overlaps this math.
         if (producer && w >= 1 && w - 1 + NST < P.nbatch) {
@@ -460,10 +466,10 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
             issue(wp + NST);
         }
 #pragma unroll
-        for (int j = 0; j < PP + DD - 1; ++j) {
-            const Stg<R> S = snext;
-            if (j + 1 < PP + DD - 1)
-                snext = widen<R>(lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W));
+        for (int j = 0; j < NJ; ++j) {
+            const Stg<R> S = sbuf[j % PF];
+            if (j + PF < NJ)
+                sbuf[j % PF] = widen<R>(lds_plain(sh_u + sh_o + (j + PF) * G::W, sh_d + sh_o + (j + PF) * G::W));
 #pragma unroll
             for (int d = 0; d < DD; ++d) {
                 const int p = j + d - (DD - 1);
