@@ -299,6 +299,7 @@ def run_gpu(args):
         "clocks": clk.summary(),
         "e2e": e2e,
         "gpu_launches": args.steps,
+        "batch_sweep": batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B),
         "g4_bytes": sl.nbytes,
         "max_g4": max_g4_capacity(dev, walkers=B),
     }
@@ -334,6 +335,32 @@ def k1_traffic(lib, n, planes, B, dtype, arith):
 SMEM_B_PER_CLK_SM = 126.0
 FP64_INSTR_PEAK = 17.0e12
 FP32_INSTR_PEAK = 35.7e12
+
+
+def batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B_main, batches=(1, 16), steps=5):
+    """Secondary points of the same K1 on the same slice (not the headline):
+    B = 1 is the HBM-bound end, B = 16 the on-chip-bound end."""
+    import torch
+    out = {}
+    for B in batches:
+        if B == B_main:
+            continue
+        gs = [T.GSigma.empty(sp, device=dev, dtype=pdtype) for _ in range(B)]
+        T.fill_gsigmas(gs, 1, [T.Origin(0, 0, w, 99, 0) for w in range(B)], "float")
+        for _ in range(2):
+            T.accumulate_g4_batch(sl, gs)
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a.record()
+        for _ in range(steps):
+            T.accumulate_g4_batch(sl, gs)
+        b.record()
+        torch.cuda.synchronize(dev)
+        s = a.elapsed_time(b) * 1e-3 / steps
+        byt = 2 * planes * n * n * eb + B * 2 * n * n * peb
+        out[str(B)] = {"updates_per_s": B * planes * n * n / s, "hbm_frac": byt / s / 1e9 / peak,
+                       "us_per_pass": s * 1e6}
+    return out
 
 
 def onchip_bounds(lib, n, planes, dtype, arith, B, upd_per_s):
