@@ -5,15 +5,18 @@ One process per GPU.  ``torch.distributed`` (gloo) is the control plane only:
 rendezvous, communicator splits, the one-time exchange of CUDA IPC handles,
 barriers.  The data path never touches the host:
 
-* payload transfers are copy-engine peer copies of the payload cores (``g4_copy_payload_cores``) straight
-  into the right neighbour's receive slot over NVLink/NVSwitch (no SM cycles);
+* payload transfers are copy-engine peer copies of the payload cores
+  (``g4_copy_payload_cores``) straight into the right neighbour's receive slot
+  over NVLink/NVSwitch (no SM cycles); the receiver rebuilds the staged halo
+  (``g4_fill_halo``) before its K1 pass;
 * ordering is carried by 64-bit sequence flags in the receiver's / sender's
   memory, written with ``cuStreamWriteValue64`` and awaited with
   ``cuStreamWaitValue64`` (``g4_flag_write`` / ``g4_flag_wait``): no host round
   trip per step, and the K1 pass over the payload received at step j runs on
   the compute stream while the comm stream forwards that same payload (and
   receives the next one);
-* the schedule of every round is the host-logic plan of ``schedule.py``;
+* the schedule of every round is the host-logic plan of ``schedule.py``; from
+  round 2 on a round is one native call (``g4_round_program_run``);
 * the end-of-run cross-sub-ring reduction sums matching slices in canonical
   rank order with a kernel that reads the peers' slices over NVLink
   (``g4_reduce_sum``), bitwise equal to the reference's ``reduce_sum``.
