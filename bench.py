@@ -300,6 +300,8 @@ def run_gpu(args):
         "e2e": e2e,
         "gpu_launches": args.steps,
         "batch_sweep": batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B),
+        "fused_arith": (fused_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B)
+                        if args.arith == "exact" else None),
         "g4_bytes": sl.nbytes,
         "max_g4": max_g4_capacity(dev, walkers=B),
     }
@@ -360,6 +362,20 @@ def batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B_main, batche
         byt = 2 * planes * n * n * eb + B * 2 * n * n * peb
         out[str(B)] = {"updates_per_s": B * planes * n * n / s, "hbm_frac": byt / s / 1e9 / peak,
                        "us_per_pass": s * 1e6}
+    return out
+
+
+def fused_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B, steps=10):
+    """The same workload in G4_ARITH_FUSED (FMA chains + deferred L2 reduction of
+    the walkers' sum; within the north_star 1e-10 tolerance, tests/ check
+    1e-12), as a secondary point: the headline stays the bitwise mode."""
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED))
+    try:
+        out = batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, 0, batches=(B,), steps=steps)[str(B)]
+    finally:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
+    out["walkers_per_pass"] = B
+    out["tolerance"] = "1e-10 relative (north_star); tests: 1e-12"
     return out
 
 

@@ -128,8 +128,10 @@ g4_status g4_set_kernel_variant(int32_t variant);
  *   G4_ARITH_EXACT (default): the reference's op order, rounding every product
  *     and sum as numpy does -> bitwise equal to ringacc on an FMA host;
  *   G4_ARITH_FUSED: the same terms as 8 fused multiply-adds chained into the
- *     accumulator -> within ~1 ulp per update (north_star tolerance 1e-10
- *     relative), bitwise for integer-valued payloads, ~1.5x fewer FP64 issues. */
+ *     accumulator; with >= 4 walkers per pass the walkers' sum is formed from
+ *     zero and added to the slice at the end with an L2 reduction (no G4 read
+ *     on the SM) -> within a few ulp (north_star tolerance 1e-10 relative),
+ *     bitwise for integer-valued payloads, ~1.5x fewer FP64 issues. */
 typedef enum { G4_ARITH_EXACT = 0, G4_ARITH_FUSED = 1 } g4_arith_mode;
 g4_status g4_set_arith_mode(int32_t mode);
 

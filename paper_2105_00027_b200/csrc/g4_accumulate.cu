@@ -320,7 +320,10 @@ struct alignas(64) TmaParams {
 // Measurement-only variants of K1 v2 (G4RING_EXP, never set in production):
 //   1 = start from zero accumulators (no G4 read)   2 = no G4 write
 //   4 = no shared-memory reads / math  (bits combine; profiles/r01_summary.md)
-enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4 };
+// K1_DEFER (production, G4_ARITH_FUSED with >= 4 walkers): the walkers' sum is
+// formed from zero and added to the slice at the end with red.global.add, so
+// no CTA waits on its G4 block (the L2 does the read-modify-write).
+enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, K1_DEFER = 16 };
 static int exp_flags() {
     static int e = -1;
     if (e < 0) {
@@ -418,7 +421,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int d = 0; d < DD; ++d) {
-            if ((EXP & EXP_NOLOAD) == 0 && (okmask & (1u << (p * DD + d)))) {
+            if ((EXP & (EXP_NOLOAD | K1_DEFER)) == 0 && (okmask & (1u << (p * DD + d)))) {
                 acc[p][d] = ld_g4(gb + p * nn + offg[d]);
             } else {
                 acc[p][d].re = R(0);
@@ -497,7 +500,13 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
 #pragma unroll
         for (int d = 0; d < DD; ++d)
             if (okmask & (1u << (p * DD + d))) {
-                if ((EXP & EXP_NOSTORE) == 0 || acc[p][d].re == R(-1234.5)) st_g4(gb + p * nn + offg[d], acc[p][d]);
+                if constexpr ((EXP & K1_DEFER) != 0) {
+                    R* a = reinterpret_cast<R*>(gb + p * nn + offg[d]);
+                    atomicAdd(a, acc[p][d].re);
+                    atomicAdd(a + 1, acc[p][d].im);
+                } else if ((EXP & EXP_NOSTORE) == 0 || acc[p][d].re == R(-1234.5)) {
+                    st_g4(gb + p * nn + offg[d], acc[p][d]);
+                }
             }
 }
 
@@ -616,6 +625,11 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
 //    8  4x4    4x4      16x16   2   1            17  8x2    2x2      16x4    4   2
 //   11  4x4    4x2      16x8    3   2            19  8x2    1x4       8x8    2   4   (default, P <= 8)
 //                                                20  4x4    2x2       8x8    2   4
+// G4_ARITH_FUSED with at least this many walkers per pass adds the walkers' sum
+// to the slice at the end (K1_DEFER): -9 % time at B = 8 and 16 (lab23); below
+// it the L2 atomics cost more than the G4 load they save.
+constexpr int DEFER_MIN_BATCH = 4;
+
 template <typename R, typename RG, bool FUSED>
 static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
     switch (g) {
@@ -637,10 +651,15 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
                     default: return fail(G4_ERR_CONTRACT, "G4RING_EXP: unknown variant");
                 }
             }
+            if (FUSED && prm.nbatch >= DEFER_MIN_BATCH)
+                return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4, FUSED ? K1_DEFER : 0>(prm, st);
             return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4>(prm, st);
         case 16: return launch_v2<R, RG, V2Geom<RG, 4, 4, 4>, FUSED, 2>(prm, st);
         case 17: return launch_v2<R, RG, V2Geom<RG, 8, 2, 4, 2, 2>, FUSED, 2>(prm, st);
-        case 19: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4>(prm, st);
+        case 19:
+            if (FUSED && prm.nbatch >= DEFER_MIN_BATCH)
+                return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4, FUSED ? K1_DEFER : 0>(prm, st);
+            return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4>(prm, st);
         case 20: return launch_v2<R, RG, V2Geom<RG, 4, 2, 2, 4, 2>, FUSED, 4>(prm, st);
         default: return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
     }

@@ -374,3 +374,36 @@ def test_core_copy_plus_halo_rebuild_is_exact(cuda_dev, n, dtype):
     _lib.check(lib.g4_fill_halo(_lib.ptr_array([dst[i].data_ptr() for i in range(k)]), k, n, code, st))
     torch.cuda.synchronize()
     assert torch.equal(torch.view_as_real(dst), torch.view_as_real(src))
+
+
+@pytest.mark.parametrize("dtype,n,lo,hi,nb", [("c128", 96, 0, 40, 6), ("c64", 96, 3, 37, 5), ("mixed", 128, 0, 24, 8),
+                                              ("c128", 128, 10, 18, 4), ("c128", 160, 0, 20, 3)])
+def test_fused_deferred_update(oracle, cuda_dev, dtype, n, lo, hi, nb):
+    """G4_ARITH_FUSED with >= 4 walkers adds the walkers' sum to a NONZERO slice
+    at the end (L2 reduction): integer payloads stay bitwise, float within
+    1e-12 (c128, mixed) / 1e-5 (c64) relative."""
+    lib = _lib.load()
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED))
+    try:
+        sp = T.CombinedIndexSpace(1, n)
+        sdt = torch.complex64 if dtype == "c64" else torch.complex128
+        gdt = torch.complex128 if dtype == "c128" else torch.complex64
+        for mode in ("integer", "float"):
+            rng = np.random.default_rng(n + nb)
+            start = (rng.integers(-3, 4, (hi - lo, n, n)) + 1j * rng.integers(-3, 4, (hi - lo, n, n)))
+            ref = start.astype(np.complex128)
+            sl = T.GtSlice(sp, lo, hi, torch.from_numpy(start.astype(np.complex128)).to(cuda_dev).to(sdt))
+            gs = [T.generate_gsigma(2, T.Origin(0, 0, w, 0, 0), sp, mode, device=cuda_dev, dtype=gdt)
+                  for w in range(nb)]
+            T.accumulate_g4_batch(sl, gs)
+            for g in gs:
+                oracle.accumulate(ref, lo, hi, to_np(g.up.contiguous()).astype(np.complex128),
+                                  to_np(g.down.contiguous()).astype(np.complex128))
+            got = to_np(sl.data).astype(np.complex128)
+            if mode == "integer":
+                assert np.array_equal(got, ref)
+            else:
+                tol = 1e-5 if dtype == "c64" else 1e-12
+                np.testing.assert_allclose(got, ref, rtol=tol, atol=tol * np.abs(ref).max())
+    finally:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
