@@ -407,3 +407,27 @@ def test_fused_deferred_update(oracle, cuda_dev, dtype, n, lo, hi, nb):
                 np.testing.assert_allclose(got, ref, rtol=tol, atol=tol * np.abs(ref).max())
     finally:
         _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
+
+
+def test_bench_workload_full_slice(oracle, cuda_dev):
+    """The bench's own N = 1 workload, checked in full (size-independent property
+    at BASELINE config 2 size): N = 512, all 64 exchange planes, one K1 pass of
+    8 device-generated walkers through the production geometry.  Integer mode
+    bitwise over every entry; float mode within 1e-13 of the numpy restatement
+    (the reference's own arithmetic), and its checksum within 1e-12."""
+    sp = T.CombinedIndexSpace(16, 32)
+    n, planes, B = sp.size, 64, 8
+    for mode in ("integer", "float"):
+        sl = T.GtSlice.zeros(sp, 0, planes, device=cuda_dev)
+        gs = [T.generate_gsigma(0, T.Origin(0, 0, w, 0, 0), sp, mode, device=cuda_dev) for w in range(B)]
+        T.accumulate_g4_batch(sl, gs)
+        ref = np.zeros((planes, n, n), np.complex128)
+        for g in gs:
+            oracle.accumulate_np(ref, 0, planes, to_np(g.up.contiguous()), to_np(g.down.contiguous()))
+        got = to_np(sl.data)
+        if mode == "integer":
+            assert np.array_equal(got, ref)
+        else:
+            scale = np.abs(ref).max()
+            np.testing.assert_allclose(got, ref, rtol=1e-13, atol=1e-13 * scale)
+            assert abs(got.sum() - ref.sum()) <= 1e-12 * np.abs(ref).sum()
