@@ -582,8 +582,8 @@ static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, in
     return G4_OK;
 }
 
-template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
-static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
+template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP>
+static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     static bool attr_set = false;
     if (!attr_set) {
         G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
@@ -616,20 +616,28 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     return G4_OK;
 }
 
-// v2 geometries: PP x DD thread block, CWQ x CWR warps (CTA tile Q x DR), NST
-// stages, CTAs per SM.  Sweep results: profiles/r01_summary.md.
-//   id  PPxDD  CWQxCWR  QxDR   NST CTA/SM       id  PPxDD  CWQxCWR  QxDR   NST CTA/SM
-//    0  4x4    4x1      16x4    3   3            12  8x4    2x2      16x8    3   2
-//    3  4x4    4x1      16x4    2   4            13  8x2    2x2      16x4    2   4   (default, P >= 16)
-//    7  4x4    4x2      16x8    2   2            16  4x4    4x1      16x4    4   2
-//    8  4x4    4x4      16x16   2   1            17  8x2    2x2      16x4    4   2
-//   11  4x4    4x2      16x8    3   2            19  8x2    1x4       8x8    2   4   (default, P <= 8)
-//                                                20  4x4    2x2       8x8    2   4
 // G4_ARITH_FUSED with at least this many walkers per pass adds the walkers' sum
 // to the slice at the end (K1_DEFER): -9 % time at B = 8 and 16 (lab23); below
 // it the L2 atomics cost more than the G4 load they save.
 constexpr int DEFER_MIN_BATCH = 4;
 
+template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
+static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
+    if constexpr (FUSED && EXP == 0) {
+        if (prm.nbatch >= DEFER_MIN_BATCH) return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER>(prm, st);
+    }
+    return launch_v2_t<R, RG, G, FUSED, MINB, EXP>(prm, st);
+}
+
+// v2 geometries: PP x DD thread block, CWQ x CWR warps (CTA tile Q x DR), NST
+// stages, CTAs per SM.  Sweep results: profiles/r01_summary.md.
+//   id  PPxDD  CWQxCWR  QxDR   NST CTA/SM       id  PPxDD  CWQxCWR  QxDR   NST CTA/SM
+//    0  4x4    4x1      16x4    3   3            12  8x4    2x2      16x8    3   2   (default, P >= 16, fused)
+//    3  4x4    4x1      16x4    2   4            13  8x2    2x2      16x4    2   4   (default, P >= 16, exact)
+//    7  4x4    4x2      16x8    2   2            16  4x4    4x1      16x4    4   2
+//    8  4x4    4x4      16x16   2   1            17  8x2    2x2      16x4    4   2
+//   11  4x4    4x2      16x8    3   2            19  8x2    1x4       8x8    2   4   (default, P <= 8)
+//                                                20  4x4    2x2       8x8    2   4
 template <typename R, typename RG, bool FUSED>
 static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
     switch (g) {
@@ -651,15 +659,10 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
                     default: return fail(G4_ERR_CONTRACT, "G4RING_EXP: unknown variant");
                 }
             }
-            if (FUSED && prm.nbatch >= DEFER_MIN_BATCH)
-                return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4, FUSED ? K1_DEFER : 0>(prm, st);
             return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2>, FUSED, 4>(prm, st);
         case 16: return launch_v2<R, RG, V2Geom<RG, 4, 4, 4>, FUSED, 2>(prm, st);
         case 17: return launch_v2<R, RG, V2Geom<RG, 8, 2, 4, 2, 2>, FUSED, 2>(prm, st);
-        case 19:
-            if (FUSED && prm.nbatch >= DEFER_MIN_BATCH)
-                return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4, FUSED ? K1_DEFER : 0>(prm, st);
-            return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4>(prm, st);
+        case 19: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4>(prm, st);
         case 20: return launch_v2<R, RG, V2Geom<RG, 4, 2, 2, 4, 2>, FUSED, 4>(prm, st);
         default: return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
     }
@@ -691,18 +694,21 @@ static bool geom_info(int g, GeomInfo* out) {
 }
 
 // Automatic choice: a 16-plane CTA tile when the slice has >= 16 planes, an
-// 8-plane tile for the 8-plane slices of an 8-GPU ring.  G4RING_V2GEOM overrides.
-static int v2_geom(int64_t planes) {
+// 8-plane tile for the 8-plane slices of an 8-GPU ring.  In G4_ARITH_FUSED the
+// G4 block is not read at CTA start (K1_DEFER), which lifts the 2-CTA/SM,
+// 32-entry-register-block geometry 12 above 13 (lab24: -7 % at B = 16, -10 %
+// at N = 4608).  G4RING_V2GEOM overrides.
+static int v2_geom(int64_t planes, bool fused) {
     static int forced = -2;
     if (forced == -2) {
         const char* e = getenv("G4RING_V2GEOM");
         forced = e ? atoi(e) : -1;
     }
     if (forced >= 0) return forced;
-    return planes >= 16 ? 13 : 19;
+    if (planes < 16) return 19;
+    return fused ? 12 : 13;
 }
 
-// ---------------------------------------------------------------------------
 static bool use_v2(int n, int64_t planes) {
     const int variant = kernel_variant();
     return n >= 64 && (variant == 2 || (variant == 0 && planes >= 4));
@@ -711,7 +717,7 @@ static bool use_v2(int n, int64_t planes) {
 template <typename R, typename RG, bool FUSED>
 static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
-    if (use_v2(prm.n, planes)) return launch_v2_geom<R, RG, FUSED>(v2_geom(planes), prm, st);
+    if (use_v2(prm.n, planes)) return launch_v2_geom<R, RG, FUSED>(v2_geom(planes, FUSED), prm, st);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
@@ -785,7 +791,8 @@ g4_status g4_k1_config(int32_t n, int64_t planes, int32_t dtype, int32_t* out) {
     if (dtype != G4_C128 && dtype != G4_C64 && dtype != G4_C128_G64) return fail(G4_ERR_CONTRACT, "unknown dtype");
     if (use_v2(n, planes)) {
         GeomInfo gi;
-        if (!geom_info(v2_geom(planes), &gi)) return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
+        if (!geom_info(v2_geom(planes, g_arith == G4_ARITH_FUSED), &gi))
+            return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
         const int32_t v[8] = {2, gi.pp, gi.dd, gi.q, gi.dr, gi.nst, gi.ctas, gi.warps};
         std::memcpy(out, v, sizeof(v));
     } else {
