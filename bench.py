@@ -622,6 +622,7 @@ def run_ring(args):
                              "lo": eng.lo, "hi": eng.hi, "host_ms": host_ms})
     e2e = run_ring_e2e(args, eng, world, dev)
     eng_native = eng.native
+    eng_wire_cores = eng.wire_cores
     eng.close()
     if rank != 0:
         return
@@ -651,6 +652,7 @@ def run_ring(args):
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
                      "kernel": "k_accumulate*", "bytes_per_launch": alg_bytes},
         "nvlink": {"bytes_per_step_per_gpu": ring_bytes,
+                   "wire": "payload cores" if eng_wire_cores else "staged payloads",
                    "achieved_gbs": ring_bytes / (ms * 1e-3) / 1e9, "peak_gbs": 770.0,
                    "peak_source": "B200_PROFILING.md measured peer copy"},
         "clocks": stats[0]["clk"],

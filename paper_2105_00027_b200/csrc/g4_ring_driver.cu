@@ -16,6 +16,7 @@
 // share pointers directly; other processes are reached through CUDA IPC.
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -71,6 +72,7 @@ struct Ring {
     int world_rank, S, pos, subring, n;
     int64_t lo, hi, next_round;
     int pcode;                 // staged payload dtype
+    bool wire_cores = true;    // cores on the wire + halo rebuild (G4RING_WIRE=staged: whole payloads)
     int64_t payload_bytes;     // one staged walker
     std::vector<Chan> chans;
     void* slice = nullptr;
@@ -178,6 +180,10 @@ g4_status g4_ring_create(const g4_ring_config* cfg, int32_t world_rank, g4_allga
     R->ctx = ctx;
     R->pcode = cfg->dtype == G4_C128 ? G4_C128 : G4_C64;
     R->payload_bytes = g4_payload_bytes(R->n, R->pcode);
+    {
+        const char* wire = getenv("G4RING_WIRE");
+        R->wire_cores = !(wire && std::strcmp(wire, "staged") == 0);
+    }
     std::vector<int64_t> ranges(2 * R->S);
     g4_status st = g4_make_partition(planes, R->S, ranges.data());
     if (st != G4_OK) {
@@ -332,7 +338,10 @@ g4_status g4_ring_measure(void* ring, int64_t m, int32_t regenerate) {
                 src = R0_BUF + (int)((k - 1) % 2);
             }
             char* dst = reinterpret_cast<char*>(R->peer_bufs[c.index]) + (R0_BUF + k % 2) * R->slot_bytes(c);
-            G4_TRY(g4_copy_payload_cores(dst, R->buf(c, src), B * (int32_t)c.lanes.size(), R->n, R->pcode, cs));
+            if (R->wire_cores)
+                G4_TRY(g4_copy_payload_cores(dst, R->buf(c, src), B * (int32_t)c.lanes.size(), R->n, R->pcode, cs));
+            else
+                G4_TRY(g4_copy_async(dst, R->buf(c, src), R->slot_bytes(c), cs));
             G4_TRY(g4_flag_write(flag(c.send_to, c.index, F_DATA), (uint64_t)k, cs));
             if (j == 0) G4_CUDA(cudaEventRecord(R->ev_sent[c.index], cs));
             if (j >= 1) G4_TRY(g4_flag_write(flag(c.recv_from, c.index, F_ACK_FWD), (uint64_t)(k - 1), cs));
@@ -343,7 +352,7 @@ g4_status g4_ring_measure(void* ring, int64_t m, int32_t regenerate) {
         for (const Chan& c : R->chans) add_slot(c, R0_BUF + (int)(k % 2));
         std::vector<void*> halo(ptrs.size());  // only the cores crossed the link
         for (size_t i = 0; i < ptrs.size(); ++i) halo[i] = const_cast<void*>(ptrs[i]);
-        G4_TRY(g4_fill_halo(halo.data(), (int32_t)halo.size(), R->n, R->pcode, R->compute));
+        if (R->wire_cores) G4_TRY(g4_fill_halo(halo.data(), (int32_t)halo.size(), R->n, R->pcode, R->compute));
         G4_TRY(k1(ptrs));
         for (const Chan& c : R->chans)
             G4_TRY(g4_flag_write(flag(c.recv_from, c.index, F_ACK_ACC), (uint64_t)k, R->compute));

@@ -266,7 +266,10 @@ class RingEngine:
         self.bufs = [torch.zeros((3, cfg.batch * len(c.lanes)) + staged_shape(n, self.pdtype), dtype=self.pdtype,
                                  device=device) for c in self.channels]
         self.payload_bytes = int(np.prod(staged_shape(n, self.pdtype))) * self.bufs[0].element_size()
-        self.wire_bytes = 2 * n * n * self.bufs[0].element_size()  # the cores that cross the link
+        # wire format: payload cores (default) or whole staged payloads (G4RING_WIRE=staged,
+        # for A/B on nodes where strided peer copies are slow; no halo rebuild then)
+        self.wire_cores = os.environ.get("G4RING_WIRE", "cores") != "staged"
+        self.wire_bytes = (2 * n * n * self.bufs[0].element_size() if self.wire_cores else self.payload_bytes)
         self.flags = torch.zeros(len(self.channels) * S.FLAGS_PER_CHANNEL, dtype=torch.int64, device=device)
         self.compute = torch.cuda.Stream(device)
         self.comm = [torch.cuda.Stream(device) for _ in self.channels]
@@ -396,13 +399,19 @@ class RingEngine:
                 c = self.channels[ci]
                 cnt = nb * len(c.lanes)
                 dst_ptr = self.peer_bufs[(peer, ci)] + dst * self.bufs[ci][0].numel() * self.bufs[ci].element_size()
-                words.append([_lib.G4_OP_COPY, sidx(st), dst_ptr, self._buf_ptr(ci, src), 0, cnt,
-                              self.space.size, self.pcode])
+                if self.wire_cores:
+                    words.append([_lib.G4_OP_COPY, sidx(st), dst_ptr, self._buf_ptr(ci, src), 0, cnt,
+                                  self.space.size, self.pcode])
+                else:
+                    words.append([_lib.G4_OP_COPY, sidx(st), dst_ptr, self._buf_ptr(ci, src),
+                                  cnt * self.payload_bytes, 0, 0, 0])
                 for t in c.lanes:
                     delta["sent"][t] += nb
                     delta["msgs"][t] += 1
                     delta["bytes"][t] += nb * self.wire_bytes
             elif kind == "halo":
+                if not self.wire_cores:
+                    continue
                 off = len(ptrs)
                 for ci, buf in op[1]:
                     ptrs += [self._buf_ptr(ci, buf, j) for j in range(nb * len(self.channels[ci].lanes))]
@@ -539,13 +548,19 @@ class RingEngine:
                 c = self.channels[ci]
                 cnt = nb * len(c.lanes)
                 dst_ptr = self.peer_bufs[(peer, ci)] + dst * self.bufs[ci][0].numel() * self.bufs[ci].element_size()
-                _lib.check(lib.g4_copy_payload_cores(dst_ptr, self._buf_ptr(ci, src), cnt, self.space.size,
-                                                     self.pcode, self._stream(st).cuda_stream), "copy_cores")
+                if self.wire_cores:
+                    _lib.check(lib.g4_copy_payload_cores(dst_ptr, self._buf_ptr(ci, src), cnt, self.space.size,
+                                                         self.pcode, self._stream(st).cuda_stream), "copy_cores")
+                else:
+                    _lib.check(lib.g4_copy_async(dst_ptr, self._buf_ptr(ci, src), cnt * self.payload_bytes,
+                                                 self._stream(st).cuda_stream), "copy")
                 for t in c.lanes:
                     self.counters[t].envelopes_sent += nb
                     self.counters[t].messages_sent += 1
                     self.counters[t].bytes_sent += nb * self.wire_bytes
             elif kind == "halo":
+                if not self.wire_cores:
+                    continue
                 ptrs = [self._buf_ptr(ci, buf, i) for ci, buf in op[1]
                         for i in range(nb * len(self.channels[ci].lanes))]
                 _lib.check(lib.g4_fill_halo(_lib.ptr_array(ptrs), len(ptrs), self.space.size, self.pcode,

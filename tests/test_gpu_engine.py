@@ -180,3 +180,15 @@ def test_native_round_program_matches_host_loop(kw, monkeypatch):
         np.testing.assert_allclose(native.tensor, ref, rtol=1e-10, atol=1e-10 * np.abs(ref).max())
     check_counts(c, native)
     assert native.lane_counters == host.lane_counters
+
+
+@pytest.mark.parametrize("wire", ["staged", "cores"])
+def test_wire_formats(wire, monkeypatch):
+    """Both ring wire formats (payload cores + halo rebuild, or whole staged
+    payloads) give the oracle's tensor, through native rounds."""
+    monkeypatch.setenv("G4RING_WIRE", wire)
+    c = cfg(world_size=3, subring_size=3, lanes=2, measurements=8, batch=2, instrument=False, n_k=4, n_w=24,
+            planes=30)
+    rep = E.run_experiment(c)
+    assert np.array_equal(rep.tensor, oracle_of(c))
+    check_counts(c, rep)
