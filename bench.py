@@ -285,6 +285,8 @@ def run_gpu(args):
         "metric": "G4 updates/s", "value": value, "unit": "updates/s", "n_gpus": 1,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "arith": args.arith,
+        "parity": ("bitwise vs the reference" if args.arith == "exact"
+                   else "within 1e-10 relative (north_star; tests 1e-12), integer payloads bitwise"),
         "data": "synthetic (reference counter-based generator on device, float mode, seed 0)",
         "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
                    "walkers_per_pass": B, "subring_size": 1, "lanes": 1,
@@ -300,8 +302,8 @@ def run_gpu(args):
         "e2e": e2e,
         "gpu_launches": args.steps,
         "batch_sweep": batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B),
-        "fused_arith": (fused_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B)
-                        if args.arith == "exact" else None),
+        "other_arith": other_arith_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B,
+                                         args.arith),
         "g4_bytes": sl.nbytes,
         "max_g4": max_g4_capacity(dev, walkers=B),
     }
@@ -365,17 +367,19 @@ def batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B_main, batche
     return out
 
 
-def fused_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B, steps=10):
-    """The same workload in G4_ARITH_FUSED (FMA chains + deferred L2 reduction of
-    the walkers' sum; within the north_star 1e-10 tolerance, tests/ check
-    1e-12), as a secondary point: the headline stays the bitwise mode."""
-    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED))
+def other_arith_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B, arith, steps=10):
+    """The same workload in the other arithmetic mode, as a secondary point.
+    exact: the reference's op order, bitwise equal to it.  fused: FMA chains
+    plus (B >= 4) the deferred L2-reduction update of the slice; within the
+    north_star 1e-10 relative (tests check 1e-12; integer payloads bitwise)."""
+    other = "exact" if arith == "fused" else "fused"
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if other == "fused" else _lib.G4_ARITH_EXACT))
     try:
         out = batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, 0, batches=(B,), steps=steps)[str(B)]
     finally:
-        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
-    out["walkers_per_pass"] = B
-    out["tolerance"] = "1e-10 relative (north_star); tests: 1e-12"
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if arith == "fused" else _lib.G4_ARITH_EXACT))
+    out.update(arith=other, walkers_per_pass=B,
+               parity="bitwise vs the reference" if other == "exact" else "1e-10 relative (north_star); tests 1e-12")
     return out
 
 
@@ -574,9 +578,12 @@ def run_ring(args):
     import torch
     import torch.distributed as dist
 
+    from paper_2105_00027_b200 import _lib
     from paper_2105_00027_b200 import engine as E
     from paper_2105_00027_b200 import tensor as T
 
+    lib = _lib.load()
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if args.arith == "fused" else _lib.G4_ARITH_EXACT))
     world = E.Control()
     rank, n_ranks = world.rank, world.size
     n_k, n_w, planes, desc = CONFIGS[args.config]
@@ -641,7 +648,7 @@ def run_ring(args):
     line = {
         "metric": "G4 updates/s", "value": value, "unit": "updates/s", "n_gpus": n_ranks,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+        "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "arith": args.arith,
         "data": "synthetic (reference counter-based generator on device, float mode, seed 0; resident)",
         "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
                    "planes_per_gpu": p_local, "walkers_per_rank_per_step": B, "subring_size": S,
@@ -728,7 +735,7 @@ def main():
     ap.add_argument("--batch", type=int, default=8, help="walkers per K1 pass (per rank)")
     ap.add_argument("--dtype", default="c128", choices=["c128", "c64", "mixed"],
                     help="mixed: complex128 G4 slice with complex64 payloads")
-    ap.add_argument("--arith", default="exact", choices=["exact", "fused"],
+    ap.add_argument("--arith", default="fused", choices=["exact", "fused"],
                     help="exact: reference op order (bitwise); fused: FMA-chained (within 1e-10)")
     ap.add_argument("--cpu-steps", type=int, default=3)
     ap.add_argument("--planes", type=int, default=0, help="override the exchange-plane count (N=1)")

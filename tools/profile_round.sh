@@ -8,7 +8,7 @@ NC="--steps 20 --warmup 5 --no-cpu-baseline"
 for dt in c64 mixed; do
   python bench.py $NC --batch $B --dtype $dt 2>/dev/null | grep -E '^\{' | tail -1 > gpurun_out/bench_${TAG}_$dt.json
 done
-python bench.py $NC --batch $B --arith fused 2>/dev/null | grep -E '^\{' | tail -1 > gpurun_out/bench_${TAG}_fused.json
+python bench.py $NC --batch $B --arith exact 2>/dev/null | grep -E "^\{" | tail -1 > gpurun_out/bench_${TAG}_exact.json
 for b in 1 16; do python bench.py $NC --batch $b 2>/dev/null | grep -E '^\{' | tail -1 > gpurun_out/bench_${TAG}_b$b.json; done
 python bench.py $NC --batch $B --planes 8 2>/dev/null | grep -E '^\{' | tail -1 > gpurun_out/bench_${TAG}_p8.json
 python bench.py --config c4 --steps 5 --warmup 3 --batch $B --no-cpu-baseline 2>/dev/null | grep -E '^\{' | tail -1 > gpurun_out/bench_${TAG}_c4.json
