@@ -323,8 +323,8 @@ def k1_traffic(lib, n, planes, B, dtype, arith):
     """DRAM bytes per K1 launch from the committed ncu capture of this exact
     launch configuration (profiles/k1_traffic.json), else None."""
     import ctypes
-    cfg = (ctypes.c_int32 * 8)()
-    lib.g4_k1_config(n, planes, {"c128": 0, "c64": 1, "mixed": 2}[dtype], cfg)
+    cfg = (ctypes.c_int32 * 9)()
+    lib.g4_k1_config(n, planes, B, {"c128": 0, "c64": 1, "mixed": 2}[dtype], cfg)
     v = list(cfg)
     key = f"v{v[0]}/{v[1]}x{v[2]}/{v[3]}x{v[4]}/{v[5]} n={n} planes={planes} B={B} {dtype} {arith}"
     try:
@@ -391,15 +391,15 @@ def onchip_bounds(lib, n, planes, dtype, arith, B, upd_per_s):
     import ctypes
     import torch
     code = {"c128": 0, "c64": 1, "mixed": 2}[dtype]
-    cfg = (ctypes.c_int32 * 8)()
-    lib.g4_k1_config(n, planes, code, cfg)
-    variant, pp, dd, q, dr, nst, ctas, warps = list(cfg)
+    cfg = (ctypes.c_int32 * 9)()
+    lib.g4_k1_config(n, planes, B, code, cfg)
+    variant, pp, dd, q, dr, nst, ctas, warps, deferred = list(cfg)
     eb = 8 if dtype == "c64" else 16          # G4 entry
     peb = 16 if dtype == "c128" else 8        # payload entry
     lds = 2 * peb * (pp + 2 * dd - 1) / (pp * dd)            # operand loads per update
     width = 32 if peb == 16 else 34
     fill = 2 * peb * width * (dr + q + dr - 1) / (q * dr * 32) if variant == 2 else 0.0  # TMA writes
-    g4 = 2 * eb / B                                          # G4 block in and out through L1
+    g4 = 0.0 if deferred else 2 * eb / B                     # G4 block in and out through L1 (deferred: L2 reduction)
     path = lds + fill + g4
     props = torch.cuda.get_device_properties(torch.cuda.current_device())
     clock_hz = 1965e6
@@ -408,7 +408,7 @@ def onchip_bounds(lib, n, planes, dtype, arith, B, upd_per_s):
     fpeak = FP32_INSTR_PEAK if dtype == "c64" else FP64_INSTR_PEAK
     return {
         "k1": {"variant": variant, "thread_block": [pp, dd], "cta_tile": [q, dr], "stages": nst,
-               "ctas_per_sm": ctas, "warps_per_cta": warps},
+               "ctas_per_sm": ctas, "warps_per_cta": warps, "deferred_update": bool(deferred)},
         "smem_path_bytes_per_update": {"operand_lds": lds, "tma_fill": fill, "g4_via_l1": g4, "total": path},
         "smem_path_achieved_TBps": path * upd_per_s / 1e12,
         "smem_path_peak_TBps": smem_peak / 1e12,

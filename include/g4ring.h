@@ -135,13 +135,15 @@ g4_status g4_set_kernel_variant(int32_t variant);
 typedef enum { G4_ARITH_EXACT = 0, G4_ARITH_FUSED = 1 } g4_arith_mode;
 g4_status g4_set_arith_mode(int32_t mode);
 
-/* The K1 configuration g4_accumulate_staged would launch for this shape (host
- * only, no GPU needed), for measurement and roofline accounting:
+/* The K1 configuration g4_accumulate_staged would launch for this shape under
+ * the current arithmetic mode (host only, no GPU needed), for measurement and
+ * roofline accounting:
  *   out[0] variant (1 = v1, 2 = v2), out[1] PP planes and out[2] DD diagonal
  *   entries per thread, out[3] Q planes and out[4] DR diagonal rows per CTA
  *   tile, out[5] shared-memory stages (0 for v1), out[6] target CTAs per SM,
- *   out[7] warps per CTA. */
-g4_status g4_k1_config(int32_t n, int64_t planes, int32_t dtype, int32_t* out);
+ *   out[7] warps per CTA, out[8] 1 if the slice update is deferred to an L2
+ *   reduction (G4_ARITH_FUSED, >= 4 walkers, >= 16 planes). */
+g4_status g4_k1_config(int32_t n, int64_t planes, int32_t nbatch, int32_t dtype, int32_t* out);
 
 /* Convenience form taking reference-layout payloads: prepares each batch into
  * `workspace` (>= g4_accumulate_workspace_bytes) then calls g4_accumulate_staged. */

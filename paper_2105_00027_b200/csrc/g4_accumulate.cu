@@ -616,15 +616,16 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     return G4_OK;
 }
 
-// G4_ARITH_FUSED with at least this many walkers per pass adds the walkers' sum
-// to the slice at the end (K1_DEFER): -9 % time at B = 8 and 16 (lab23); below
-// it the L2 atomics cost more than the G4 load they save.
-constexpr int DEFER_MIN_BATCH = 4;
+// G4_ARITH_FUSED adds the walkers' sum to the slice at the end (K1_DEFER) with
+// >= 4 walkers per pass on >= 16 planes: -9 % time at B = 8 and 16 (lab23).
+// With fewer walkers, or on the small slices of an 8-GPU ring, the L2 atomics
+// cost more than the G4 load they save (r01f: B = 1 and P = 8 lines).
+static bool defer_update(int nbatch, int64_t planes) { return nbatch >= 4 && planes >= 16; }
 
 template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
 static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     if constexpr (FUSED && EXP == 0) {
-        if (prm.nbatch >= DEFER_MIN_BATCH) return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER>(prm, st);
+        if (defer_update(prm.nbatch, prm.hi - prm.lo)) return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER>(prm, st);
     }
     return launch_v2_t<R, RG, G, FUSED, MINB, EXP>(prm, st);
 }
@@ -694,11 +695,11 @@ static bool geom_info(int g, GeomInfo* out) {
 }
 
 // Automatic choice: a 16-plane CTA tile when the slice has >= 16 planes, an
-// 8-plane tile for the 8-plane slices of an 8-GPU ring.  In G4_ARITH_FUSED the
-// G4 block is not read at CTA start (K1_DEFER), which lifts the 2-CTA/SM,
-// 32-entry-register-block geometry 12 above 13 (lab24: -7 % at B = 16, -10 %
-// at N = 4608).  G4RING_V2GEOM overrides.
-static int v2_geom(int64_t planes, bool fused) {
+// 8-plane tile for the 8-plane slices of an 8-GPU ring.  When the G4 block is
+// not read at CTA start (K1_DEFER), the 2-CTA/SM, 32-entry-register-block
+// geometry 12 beats 13 (lab24: -7 % at B = 16, -10 % at N = 4608).
+// G4RING_V2GEOM overrides.
+static int v2_geom(int64_t planes, bool deferred) {
     static int forced = -2;
     if (forced == -2) {
         const char* e = getenv("G4RING_V2GEOM");
@@ -706,7 +707,7 @@ static int v2_geom(int64_t planes, bool fused) {
     }
     if (forced >= 0) return forced;
     if (planes < 16) return 19;
-    return fused ? 12 : 13;
+    return deferred ? 12 : 13;
 }
 
 static bool use_v2(int n, int64_t planes) {
@@ -717,7 +718,8 @@ static bool use_v2(int n, int64_t planes) {
 template <typename R, typename RG, bool FUSED>
 static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
-    if (use_v2(prm.n, planes)) return launch_v2_geom<R, RG, FUSED>(v2_geom(planes, FUSED), prm, st);
+    if (use_v2(prm.n, planes))
+        return launch_v2_geom<R, RG, FUSED>(v2_geom(planes, FUSED && defer_update(prm.nbatch, planes)), prm, st);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
@@ -784,21 +786,22 @@ g4_status g4_set_kernel_variant(int32_t variant) {
     return G4_OK;
 }
 
-g4_status g4_k1_config(int32_t n, int64_t planes, int32_t dtype, int32_t* out) {
+g4_status g4_k1_config(int32_t n, int64_t planes, int32_t nbatch, int32_t dtype, int32_t* out) {
     using namespace g4;
     if (!out) return fail(G4_ERR_CONTRACT, "k1_config: null output");
-    if (n < 1 || planes < 1) return fail(G4_ERR_CONTRACT, "k1_config: n and planes must be >= 1");
+    if (n < 1 || planes < 1 || nbatch < 1) return fail(G4_ERR_CONTRACT, "k1_config: n, planes and nbatch must be >= 1");
     if (dtype != G4_C128 && dtype != G4_C64 && dtype != G4_C128_G64) return fail(G4_ERR_CONTRACT, "unknown dtype");
+    const int32_t walkers = std::min<int32_t>(nbatch, TMA_MAXW);  // per launch
     if (use_v2(n, planes)) {
+        const bool deferred = g_arith == G4_ARITH_FUSED && defer_update(walkers, planes);
         GeomInfo gi;
-        if (!geom_info(v2_geom(planes, g_arith == G4_ARITH_FUSED), &gi))
-            return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
-        const int32_t v[8] = {2, gi.pp, gi.dd, gi.q, gi.dr, gi.nst, gi.ctas, gi.warps};
+        if (!geom_info(v2_geom(planes, deferred), &gi)) return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
+        const int32_t v[9] = {2, gi.pp, gi.dd, gi.q, gi.dr, gi.nst, gi.ctas, gi.warps, deferred ? 1 : 0};
         std::memcpy(out, v, sizeof(v));
     } else {
         const int warps = planes <= 4 ? 1 : planes <= 8 ? 2 : 4;
         const int ctas = planes <= 4 ? 12 : planes <= 8 ? 6 : 3;
-        const int32_t v[8] = {1, 4, 4, 4 * warps, 4, 0, ctas, warps};
+        const int32_t v[9] = {1, 4, 4, 4 * warps, 4, 0, ctas, warps, 0};
         std::memcpy(out, v, sizeof(v));
     }
     return G4_OK;

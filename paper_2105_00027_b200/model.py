@@ -248,14 +248,15 @@ class K1Calibration:
 B200_K1 = K1Calibration()
 
 
-def k1_geometry(n: int, planes: int, dtype: str) -> dict:
-    """The launch g4_accumulate_staged picks for this shape (g4_k1_config)."""
+def k1_geometry(n: int, planes: int, dtype: str, nbatch: int = 8) -> dict:
+    """The launch g4_accumulate_staged picks for this shape under the current
+    arithmetic mode (g4_k1_config)."""
     _check_dtype(dtype)
-    out = (ctypes.c_int32 * 8)()
-    _lib.check(_lib.load().g4_k1_config(n, planes, _DTYPE[dtype], out), "k1_config")
+    out = (ctypes.c_int32 * 9)()
+    _lib.check(_lib.load().g4_k1_config(n, planes, nbatch, _DTYPE[dtype], out), "k1_config")
     v = list(out)
     return {"variant": v[0], "pp": v[1], "dd": v[2], "q": v[3], "dr": v[4], "stages": v[5],
-            "ctas_per_sm": v[6], "warps": v[7]}
+            "ctas_per_sm": v[6], "warps": v[7], "deferred": bool(v[8])}
 
 
 def k1_pass_time(n: int, planes: int, batch: int, dtype: str = "c128", arith: str = "exact",
@@ -263,14 +264,14 @@ def k1_pass_time(n: int, planes: int, batch: int, dtype: str = "c128", arith: st
     """Modelled time of one K1 launch (B walkers over a P-plane slice) and its bounds."""
     if min(n, planes, batch) < 1:
         raise ContractViolation("k1_pass_time arguments must be >= 1")
-    g = k1_geometry(n, planes, dtype)
+    g = k1_geometry(n, planes, dtype, batch)
     eb, peb = entry_bytes(dtype), payload_entry_bytes(dtype)
     upd = batch * planes * n * n
     hbm_b = 2 * planes * n * n * eb + batch * 2 * n * n * peb
     lds = 2 * peb * (g["pp"] + 2 * g["dd"] - 1) / (g["pp"] * g["dd"])
     width = 32 if peb == 16 else 34
     fill = 2 * peb * width * (g["dr"] + g["q"] + g["dr"] - 1) / (g["q"] * g["dr"] * 32) if g["variant"] == 2 else 0.0
-    smem_b = upd * (lds + fill + 2 * eb / batch)
+    smem_b = upd * (lds + fill + (0.0 if g["deferred"] else 2 * eb / batch))
     fp_i = upd * (8 if arith == "fused" else 12)
     fpeak = cal.fp32_instr_per_s if dtype == "c64" else cal.fp64_instr_per_s
     # wave quantisation: the last wave of CTAs leaves SMs idle

@@ -93,16 +93,23 @@ def test_k1_config_host_query():
     """g4_k1_config (host only): the launch g4_accumulate_staged picks per shape."""
     lib = _lib.load()
 
-    def cfg(n, planes, dtype=_lib.G4_C128):
-        out = (ctypes.c_int32 * 8)()
-        _lib.check(lib.g4_k1_config(n, planes, dtype, out))
+    def cfg(n, planes, dtype=_lib.G4_C128, nbatch=8):
+        out = (ctypes.c_int32 * 9)()
+        _lib.check(lib.g4_k1_config(n, planes, nbatch, dtype, out))
         return list(out)
 
     assert cfg(512, 64)[:5] == [2, 8, 2, 16, 4]      # 16-plane CTA tile
     assert cfg(512, 8)[:5] == [2, 8, 2, 8, 8]        # 8-plane tile for an 8-GPU share
     assert cfg(512, 2)[0] == 1 and cfg(32, 64)[0] == 1  # v1: < 4 planes or N < 64
     assert cfg(4608, 72, _lib.G4_C128_G64)[0] == 2
+    assert cfg(512, 64)[8] == 0                         # exact mode: slice read and written by K1
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED))
+    try:
+        assert cfg(512, 64)[:5] == [2, 8, 4, 16, 8] and cfg(512, 64)[8] == 1   # deferred update, geometry 12
+        assert cfg(512, 64, nbatch=2)[8] == 0 and cfg(512, 8)[8] == 0          # not for B < 4 or P < 16
+    finally:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
     with pytest.raises(errors.ContractViolation):
-        _lib.check(lib.g4_k1_config(0, 8, _lib.G4_C128, (ctypes.c_int32 * 8)()))
+        _lib.check(lib.g4_k1_config(0, 8, 8, _lib.G4_C128, (ctypes.c_int32 * 9)()))
     with pytest.raises(errors.ContractViolation):
-        _lib.check(lib.g4_k1_config(512, 8, 7, (ctypes.c_int32 * 8)()))
+        _lib.check(lib.g4_k1_config(512, 8, 8, 7, (ctypes.c_int32 * 9)()))
