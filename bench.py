@@ -341,23 +341,26 @@ FP64_INSTR_PEAK = 17.0e12
 FP32_INSTR_PEAK = 35.7e12
 
 
-def batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B_main, batches=(1, 16), steps=5):
-    """Secondary points of the same K1 on the same slice (not the headline):
-    B = 1 is the HBM-bound end, B = 16 the on-chip-bound end."""
+def batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B_main, batches=(1, 16), steps=6):
+    """Secondary points of the same K1 on the same slice (not the headline),
+    timed like the headline: two walker pools alternate, so no step re-reads
+    the previous step's L2-resident payloads.  B = 1 is the HBM-bound end,
+    B = 16 the on-chip-bound end."""
     import torch
     out = {}
     for B in batches:
         if B == B_main:
             continue
-        gs = [T.GSigma.empty(sp, device=dev, dtype=pdtype) for _ in range(B)]
-        T.fill_gsigmas(gs, 1, [T.Origin(0, 0, w, 99, 0) for w in range(B)], "float")
-        for _ in range(2):
-            T.accumulate_g4_batch(sl, gs)
+        pools = [[T.GSigma.empty(sp, device=dev, dtype=pdtype) for _ in range(B)] for _ in range(2)]
+        for i, pool in enumerate(pools):
+            T.fill_gsigmas(pool, 1, [T.Origin(0, 0, w, 90 + i, 0) for w in range(B)], "float")
+        for i in range(4):
+            T.accumulate_g4_batch(sl, pools[i % 2])
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         a.record()
-        for _ in range(steps):
-            T.accumulate_g4_batch(sl, gs)
+        for i in range(steps):
+            T.accumulate_g4_batch(sl, pools[i % 2])
         b.record()
         torch.cuda.synchronize(dev)
         s = a.elapsed_time(b) * 1e-3 / steps

@@ -729,7 +729,13 @@ static int g_arith = G4_ARITH_EXACT;
 
 template <typename R, typename RG>
 static g4_status dispatch(const AccParams<R, RG>& prm, cudaStream_t st) {
-    return g_arith == G4_ARITH_FUSED ? dispatch_t<R, RG, true>(prm, st) : dispatch_t<R, RG, false>(prm, st);
+    // G4_ARITH_FUSED pays off through the deferred update; where that does not
+    // apply (few walkers, small slices, v1) the exact kernel is as fast, so it
+    // runs instead (and stays bitwise).
+    const int64_t planes = prm.hi - prm.lo;
+    const bool fused = g_arith == G4_ARITH_FUSED && use_v2(prm.n, planes) &&
+                       defer_update(std::min<int32_t>(prm.nbatch, TMA_MAXW), planes);
+    return fused ? dispatch_t<R, RG, true>(prm, st) : dispatch_t<R, RG, false>(prm, st);
 }
 
 template <typename R, typename RG>
