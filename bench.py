@@ -257,21 +257,21 @@ def run_gpu(args):
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
-    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-          for _ in range(args.steps)]
+    # The timed region holds only K1 launches, back to back on `stream`: their
+    # mean duration is the region's event time / steps (gaps included, so
+    # conservative).  Per-launch event pairs would serialise consecutive K1
+    # launches (+5 us per pass, tools/loop_ab.py).
     t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         time.sleep(0.3)  # let the sampler start
         torch.cuda.synchronize()
         t_start.record(stream)
         for i in range(args.steps):
-            ev[i][0].record(stream)
             step(i)
-            ev[i][1].record(stream)
         t_end.record(stream)
         torch.cuda.synchronize()
     total_ms = t_start.elapsed_time(t_end)
-    k_ms = [a.elapsed_time(b) for a, b in ev]
+    k_ms = [total_ms / args.steps]
     upd_step = B * planes * n * n
     value = upd_step * args.steps / (total_ms * 1e-3)
     peak, peak_kind = measured_peaks()
