@@ -254,8 +254,15 @@ def run_gpu(args):
     def step(i):
         T.accumulate_g4_batch(sl, pools[i % 2])
 
-    for i in range(args.warmup):
+    # W warm-up steps, continued to >= 0.5 s of GPU work so that a cold GPU's
+    # clocks and the L2 reach steady state before timing
+    t_w = time.perf_counter()
+    i = 0
+    while i < args.warmup or time.perf_counter() - t_w < 0.5:
         step(i)
+        i += 1
+        if i % 8 == 0:
+            torch.cuda.synchronize()
     torch.cuda.synchronize()
     # The timed region holds only K1 launches, back to back on `stream`: their
     # mean duration is the region's event time / steps (gaps included, so
