@@ -15,6 +15,7 @@
 #include <vector>
 
 #include <cuda.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "g4_common.cuh"
 #include "g4_internal.h"
@@ -369,6 +370,15 @@ g4_status g4_round_program_run(void* prog, int64_t m, int32_t regenerate) {
     using namespace g4;
     auto* P = static_cast<RoundProgram*>(prog);
     if (!P || m < 0) return fail(G4_ERR_CONTRACT, "round_program_run: bad arguments");
+    // host-side range for nsys / Nsight timelines (no cost without a tool)
+    struct Range {
+        explicit Range(int64_t m) {
+            char name[48];
+            snprintf(name, sizeof(name), "g4 round %lld", (long long)m);
+            nvtxRangePushA(name);
+        }
+        ~Range() { nvtxRangePop(); }
+    } range(m);
     int acc = 0;
     std::vector<int64_t> meas;
     for (size_t i = 0; i < P->ops.size(); i += G4_OP_WORDS) {

@@ -23,6 +23,7 @@
 #include <vector>
 
 #include <unistd.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "g4_internal.h"
 #include "g4_layout.h"
@@ -287,6 +288,10 @@ g4_status g4_ring_measure(void* ring, int64_t m, int32_t regenerate) {
         return G4_ERR_CONTRACT;
     }
     R->next_round = m + 1;
+    nvtxRangePushA("g4 ring round");
+    struct Pop {
+        ~Pop() { nvtxRangePop(); }
+    } pop;
     const int S = R->S, B = R->cfg.batch;
     const int64_t steps = S - 1;
     auto flag = [&](int pos, int ci, int f) {
