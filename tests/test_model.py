@@ -109,3 +109,21 @@ def test_cli_runs(capsys):
     M.main(["--config", "c2"])
     out = capsys.readouterr().out
     assert "c2 c128" in out and "ring-bound" in out
+
+
+def test_model_geometry_matches_library_launch():
+    """The K1 model reads its geometry from the library (g4_k1_config), so the
+    byte counts it prices are those of the launch that actually runs."""
+    g = M.k1_geometry(512, 64, "c128", 8)
+    assert (g["variant"], g["pp"], g["dd"], g["q"], g["dr"]) == (2, 8, 2, 16, 4)
+    assert not g["deferred"]
+    g8 = M.k1_geometry(512, 8, "c128", 8)
+    assert (g8["q"], g8["dr"]) == (8, 8)
+    small = M.k1_geometry(32, 1, "c128", 16)
+    assert small["variant"] == 1
+
+
+def test_wire_bytes_are_payload_cores():
+    assert M.wire_payload_bytes(512, "c128") == 2 * 512 * 512 * 16
+    assert M.wire_payload_bytes(512, "mixed") == 2 * 512 * 512 * 8
+    assert M.staged_payload_bytes(512, "c128") > M.wire_payload_bytes(512, "c128")
