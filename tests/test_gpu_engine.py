@@ -192,3 +192,13 @@ def test_wire_formats(wire, monkeypatch):
     rep = E.run_experiment(c)
     assert np.array_equal(rep.tensor, oracle_of(c))
     check_counts(c, rep)
+
+
+def test_verify_harness_like_reference():
+    """accuracy.verify (accuracy.py:108-128): float-mode ring runs pass the
+    5e-7 gate for every seed; the corrupt negative control fails it."""
+    from paper_2105_00027_b200 import accuracy as A
+    c = cfg(world_size=2, subring_size=2, lanes=2, measurements=3, value_mode="float", n_k=4, n_w=8)
+    res = A.verify(c, runs=2)
+    assert res.passed and len(res.reports) == 2 and res.mean("l2_real") < 1e-12
+    assert not A.verify(c, runs=1, corrupt=True).passed

@@ -89,3 +89,24 @@ def test_c64_oracle_close_to_c128(oracle):
     oracle.accumulate(a, 4, 7, up, down)
     oracle.accumulate(b, 4, 7, up, down)
     assert oracle.compare(a, b)["l2_real"] < 1e-6
+
+
+def test_accuracy_metrics_match_reference_definitions():
+    """paper_2105_00027_b200.accuracy restates ringacc.accuracy's metrics
+    (accuracy.py:23-64) on numpy or torch tensors (CPU here)."""
+    import numpy as np
+    import pytest as _pt
+    from paper_2105_00027_b200 import accuracy as A
+    rng = np.random.default_rng(3)
+    ref = rng.standard_normal((3, 4, 4)) + 1j * rng.standard_normal((3, 4, 4))
+    test = ref + 1e-9 * (rng.standard_normal(ref.shape) + 1j * rng.standard_normal(ref.shape))
+    r = A.compare(ref, test)
+    want_l1 = np.abs(ref.real - test.real).sum() / np.abs(ref.real).sum()
+    want_l2 = np.sqrt((np.abs(ref.imag - test.imag) ** 2).sum() / (np.abs(ref.imag) ** 2).sum())
+    assert r.l1_real == _pt.approx(want_l1, rel=1e-12) and r.l2_imag == _pt.approx(want_l2, rel=1e-12)
+    assert r.passed and A.compare(ref, ref).to_dict()["pass"]
+    bad = test.copy()
+    bad.flat[0] += 1 + 1j
+    assert not A.compare(ref, bad).passed
+    with _pt.raises(A.UndefinedNormError):
+        A.l1_error(np.zeros(4), np.ones(4))
