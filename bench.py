@@ -695,35 +695,56 @@ def ring_model_line(n, planes, gpus, batch, dtype, subring_size, lanes):
 
 def run_ring_e2e(args, eng, world, dev):
     """Ring e2e: each rank's walkers arrive in pinned host memory (reference
-    layout); per step H2D + stage (K2) + round + D2H of a probe row."""
+    layout); per step H2D (double-buffered on a copy stream, overlapping the
+    previous round) + stage (K2) + round + D2H of a probe row."""
     import torch
     B = args.batch * eng.cfg.lanes  # walkers staged per rank per round (all lanes)
     n = eng.space.size
     dtype = eng.dtype
     ups = [torch.randn(n, n, dtype=dtype).pin_memory() for _ in range(B)]
     downs = [torch.randn(n, n, dtype=dtype).pin_memory() for _ in range(B)]
-    dups = [torch.empty((n, n), dtype=dtype, device=dev) for _ in range(B)]
-    ddowns = [torch.empty((n, n), dtype=dtype, device=dev) for _ in range(B)]
+    dev_bufs = [([torch.empty((n, n), dtype=dtype, device=dev) for _ in range(B)],
+                 [torch.empty((n, n), dtype=dtype, device=dev) for _ in range(B)]) for _ in range(2)]
     probe = torch.empty(n, dtype=dtype).pin_memory()
+    copy = torch.cuda.Stream(dev)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    for j in range(2):
+        done[j].record(eng.compute)
     eng.kernel_events = None
 
-    def step(i):
-        with torch.cuda.stream(eng.compute):
+    def h2d(i):
+        j = i % 2
+        with torch.cuda.stream(copy):
+            copy.wait_event(done[j])
             for w in range(B):
-                dups[w].copy_(ups[w], non_blocking=True)
-                ddowns[w].copy_(downs[w], non_blocking=True)
-            eng.stage_gen(dups, ddowns)
+                dev_bufs[j][0][w].copy_(ups[w], non_blocking=True)
+                dev_bufs[j][1][w].copy_(downs[w], non_blocking=True)
+            ready[j].record(copy)
+
+    def step(i):
+        j = i % 2
+        with torch.cuda.stream(eng.compute):
+            eng.compute.wait_event(ready[j])
+            eng.stage_gen(dev_bufs[j][0], dev_bufs[j][1])
+            done[j].record(eng.compute)
             eng.enqueue_round(regenerate=False)
             probe.copy_(eng.slice.data[0, 0], non_blocking=True)
 
+    h2d(0)
     for i in range(2):
+        h2d(i + 1)
         step(i)
     eng.wait_idle(120.0)
     world.barrier()
     torch.cuda.synchronize(dev)
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(eng.compute)
+    copy.wait_event(t0)
+    h2d(2)
     for i in range(args.steps):
+        if i + 1 < args.steps:
+            h2d(3 + i)
         step(2 + i)
     t1.record(eng.compute)
     eng.wait_idle(300.0)
@@ -732,7 +753,8 @@ def run_ring_e2e(args, eng, world, dev):
     eb = 16 if dtype == torch.complex128 else 8
     return {"value": world.size * B * eng.cfg.num_planes * n * n / (ms * 1e-3),  # B includes lanes
             "unit": "updates/s", "h2d_bytes_per_step": B * 2 * n * n * eb, "d2h_bytes_per_step": n * eb,
-            "path": "pinned host walkers -> H2D -> g4_prepare_g (K2) -> ring round; D2H probe row"}
+            "path": "pinned host walkers -> H2D (copy stream, double-buffered) -> g4_prepare_g (K2) "
+                    "-> ring round; D2H probe row"}
 
 
 def main():

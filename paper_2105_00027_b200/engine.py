@@ -579,6 +579,11 @@ class RingEngine:
                 for i in range(self.cfg.batch * len(c.lanes))]
         if len(ups) != len(ptrs) or len(downs) != len(ptrs):
             raise ContractViolation(f"expected {len(ptrs)} payloads, got {len(ups)}")
+        # GEN of the previous round must have left (its first ring copy) before it is overwritten
+        for c in self.channels:
+            ev = self.events.get(f"sent{c.index}")
+            if ev is not None:
+                self.compute.wait_event(ev)
         code_in = _dtype_code(ups[0].dtype)
         _lib.check(self.lib.g4_prepare_g(_lib.ptr_array(ptrs), _lib.ptr_array([u.data_ptr() for u in ups]),
                                          _lib.ptr_array([d.data_ptr() for d in downs]), len(ptrs),
