@@ -271,6 +271,33 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
 }
+// Same, delivered to every CTA of the cluster in `mask` (same smem offsets and
+// mbarrier offset in each destination CTA).
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                               uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "h"(mask)
+        : "memory");
+}
+// Arrive on the mbarrier at the same offset in cluster CTA `rank` (default
+// .release.cta semantics: a .cluster-scope release costs a MEMBAR per arrive,
+// 3.7 stall cycles per issue in the first cut).
+__device__ __forceinline__ void mbar_arrive_remote(uint64_t* b, uint32_t rank) {
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %0, %1;\n\t"
+        "mbarrier.arrive.shared::cluster.b64 _, [ra];\n}" ::"r"(smem_u32(b)),
+        "r"(rank)
+        : "memory");
+}
+// Cluster barrier without a release fence: the mbarrier inits it publishes are
+// ordered by fence.mbarrier_init.release.cluster (an .arrive.release would add
+// a MEMBAR.GPU, ~2 us per CTA behind in-flight global traffic).
+__device__ __forceinline__ void cluster_sync_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;\n\tbarrier.cluster.wait.aligned;" ::: "memory");
+}
 constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel params)
 
 // Geometry of one v2 configuration.  A thread owns PP planes x DD diagonal
@@ -280,28 +307,43 @@ constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel 
 // e < DR).  Per walker the CTA fetches DR direct rows and Q + DR - 1 band rows
 // (32 entries x 2 spins each): (Q + 2 DR - 1) / (Q DR) rows per G4 entry.
 // NST-stage shared-memory ring, payload entry type R.
-template <typename R, int PP_, int CW_, int NST_, int DD_ = 4, int CWR_ = 1, int PF_ = 1>
+//
+// CL > 1: diagonal clusters.  The CL CTAs of a cluster own consecutive plane
+// chunks x with their (K1, K2) tiles shifted by Q per chunk, i.e. tiles
+// (q0 + r Q, k1_0 + r Q, j0 + r Q), r < CL.  The shifted band depends only on
+// (k1 - q, k2 - q), so all CL CTAs need the SAME band: each loads HS = NSH / CL
+// of its rows and multicasts them to the whole cluster (TMA .multicast::cluster),
+// cutting the L2 -> SM band traffic by CL.  Needs N % 32 == 0 and chunks % CL == 0.
+template <typename R, int PP_, int CW_, int NST_, int DD_ = 4, int CWR_ = 1, int PF_ = 1, int CL_ = 1>
 struct V2Geom {
     static constexpr int PP = PP_, DD = DD_, CWQ = CW_, CWR = CWR_, NST = NST_;
     static constexpr int PF = PF_;  // shifted operands loaded this many diagonals ahead
+    static constexpr int CL = CL_;  // CTAs per cluster (band multicast)
+    using Base = V2Geom<R, PP_, CW_, NST_, DD_, CWR_, PF_, 1>;
     static constexpr int CW = CWQ * CWR;                          // warps per CTA
     static constexpr int Q = PP * CWQ, DR = DD * CWR;             // CTA tile: planes x diagonal entries
     static constexpr int ES = sizeof(Cx<R>);                      // bytes per complex entry
     static constexpr int NSH = Q + DR - 1;                        // shifted row segments (band height)
+    // Band rows loaded per cluster CTA.  Each CTA's slice must start 128-B aligned
+    // in shared memory: complex64 rows are 34 x 8 = 272 B, so 8-row granules.
+    static constexpr int HS_ALIGN = (ES == 8 && CL > 1) ? 8 : 1;
+    static constexpr int HS = ((NSH + CL - 1) / CL + HS_ALIGN - 1) / HS_ALIGN * HS_ALIGN;
+    static constexpr int SH_ROWS = HS * CL;                       // band rows held (>= NSH)
     // Box row width in entries.  A TMA box must start on a 16-B boundary along
     // its innermost dimension (tools/tma_probe.cu: odd 8-B starts fault), so for
     // complex64 boxes start at the even entry below and carry 2 extra entries;
     // consumers add the start's parity (0 or 1).
     static constexpr int W = ES == 8 ? 34 : 32;
     static constexpr int DIR_ELEMS = DR * W;                      // per spin (sheared direct box)
-    static constexpr int SH_ELEMS = NSH * W;                      // per spin
+    static constexpr int SH_ELEMS = SH_ROWS * W;                  // per spin
     static constexpr uint32_t DIR_BYTES = 2 * DIR_ELEMS * ES;     // both spins
     static constexpr uint32_t SH_BYTES = 2 * SH_ELEMS * ES;
     static constexpr uint32_t DIR_OFF = 0;
     static constexpr uint32_t SH_OFF = (DIR_BYTES + 127) / 128 * 128;
     static constexpr uint32_t STAGE_BYTES = (SH_OFF + SH_BYTES + 127) / 128 * 128;
     static constexpr size_t SMEM = (size_t)NST * STAGE_BYTES + 2 * NST * sizeof(uint64_t);
-    static_assert(NSH <= G4_HALO_ROWS && NSH + W + 1 < G4_HALO_COLS, "halo too small for the v2 band");
+    static_assert(SH_ROWS <= G4_HALO_ROWS && NSH + W + 1 < G4_HALO_COLS, "halo too small for the v2 band");
+    static_assert(SH_ROWS + W + 1 < G4_HALO_COLS && DR + W <= G4_HALO_COLS, "halo too small for the v2 boxes");
     static_assert(SMEM <= 227 * 1024, "v2 stages exceed shared memory");
 };
 
@@ -368,10 +410,13 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int DR = G::DR, Q = G::Q;
+    constexpr int CL = G::CL;
     const TileCoord tc = tile_coord(blockIdx.x, P.nx, (n + 31) / 32, (n + DR - 1) / DR);
     const int64_t q0 = P.lo + (int64_t)tc.x * Q;
-    const int j0 = tc.y * 32;
-    const int k1_0 = tc.z * DR;
+    // cluster rank = chunk index mod CL (tile_coord runs x fastest; nx % CL == 0)
+    const int crank = CL > 1 ? tc.x % CL : 0;
+    const int j0 = CL > 1 ? wrap(tc.y * 32 + crank * Q, n) : tc.y * 32;
+    const int k1_0 = CL > 1 ? wrap(tc.z * DR + crank * Q, n) : tc.z * DR;
     const bool producer = threadIdx.x == 0;
     // Sheared coordinates (c1, c2) address stg[c2][c1 - off + c2].
     //  direct tile: rows k1_0 + i, columns j0 + i + j      -> (j0 - k1_0 + off, k1_0)
@@ -386,23 +431,47 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
         unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
         tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), k1_0, 0, &full[s]);
-        tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
+        if constexpr (CL == 1) {
+            tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
+        } else {  // this CTA's HS band rows, per spin, to every CTA of the cluster
+#pragma unroll
+            for (int spin = 0; spin < 2; ++spin)
+                tma_load_3d_mc(st + G::SH_OFF + (size_t)(spin * G::SH_ELEMS + crank * G::HS * G::W) * G::ES,
+                               &P.smap[w], EW * (xs - ps), R0 + crank * G::HS, spin, &full[s],
+                               (uint16_t)((1u << CL) - 1));
+        }
+    };
+    // A warp is done with stage s: release it in every CTA that multicasts into it.
+    auto release = [&](int s) {
+        __syncwarp();
+        if constexpr (CL == 1) {
+            if (lane == 0) mbar_arrive(&empty[s]);
+        } else if (lane < CL) {  // lane r releases the stage in cluster CTA r
+            mbar_arrive_remote(&empty[s], (uint32_t)lane);
+        }
     };
 
     if (producer) {
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], G::CW);
+            mbar_init(&empty[s], G::CW * CL);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int w = 0; w < NST && w < P.nbatch; ++w) issue(w);
+        if constexpr (CL == 1)
+            for (int w = 0; w < NST && w < P.nbatch; ++w) issue(w);
     }
-    __syncthreads();
+    if constexpr (CL == 1) {
+        __syncthreads();
+    } else {  // every CTA's barriers exist before any multicast lands
+        cluster_sync_relaxed();
+        if (producer)
+            for (int w = 0; w < NST && w < P.nbatch; ++w) issue(w);
+    }
 
     // ---- warp (wq, wr) owns planes q0 + PP*wq + p and diagonal entries e = DD*wr + d ----
     const int wq = warp % G::CWQ, wr = warp / G::CWQ;
     const int c = j0 + lane;
-    const bool col_ok = c < n;
+    const bool col_ok = CL > 1 || c < n;  // shifted cluster tiles wrap (N % 32 == 0)
     const int64_t nn = (int64_t)n * n;
     const int64_t qw = q0 + PP * wq;
     const int e0 = DD * wr;
@@ -415,7 +484,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     for (int p = 0; p < PP; ++p)
 #pragma unroll
         for (int d = 0; d < DD; ++d)
-            if (col_ok && (qw + p) < P.hi && (k1_0 + e0 + d) < n) okmask |= 1u << (p * DD + d);
+            if (col_ok && (qw + p) < P.hi && (CL > 1 || (k1_0 + e0 + d) < n)) okmask |= 1u << (p * DD + d);
     Cx<R> acc[PP][DD];
 #pragma unroll
     for (int p = 0; p < PP; ++p)
@@ -446,8 +515,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
                 mbar_wait(&empty[(w - 1) % NST], ((w - 1) / NST) & 1);
                 issue(w - 1 + NST);
             }
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            release(s);
             continue;
         }
         // Direct elements first (sheared box: row d, column lane); shifted elements
@@ -491,8 +559,15 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         }
         // Release the stage only once its values have been consumed by the math
         // (an in-flight ld.shared must not race the TMA refill of the stage).
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        release(s);
+    }
+    // Peers arrive on this CTA's empty barriers until they finish their last
+    // walkers: the producer waits for those final phases, so no remote arrive
+    // can land after the CTA (and its shared memory) is gone.
+    if constexpr (CL > 1) {
+        if (producer)
+            for (int w = P.nbatch > NST ? P.nbatch - NST : 0; w < P.nbatch; ++w)
+                mbar_wait(&empty[w % NST], (w / NST) & 1);
     }
 
 #pragma unroll
@@ -536,7 +611,8 @@ static PFN_encodeTiled tensor_map_encoder() {
     return encode;
 }
 
-static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, int dd, MapPair* out) {
+static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, int dd, int band_spins,
+                           MapPair* out) {
     PFN_encodeTiled encode = tensor_map_encoder();
     if (!encode) return fail(G4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     const cuuint64_t ld = (cuuint64_t)staged_ld(n, es), rows = (cuuint64_t)staged_rows(n, es);
@@ -553,7 +629,8 @@ static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, i
     const cuuint32_t estr[3] = {1, 1, 1};
     void* base = static_cast<char*>(const_cast<void*>(stg)) - (size_t)off * es;
     for (int which = 0; which < 2; ++which) {
-        const cuuint32_t box[3] = {(cuuint32_t)width * ew, which == 0 ? (cuuint32_t)dd : (cuuint32_t)nsh, 2};
+        const cuuint32_t box[3] = {(cuuint32_t)width * ew, which == 0 ? (cuuint32_t)dd : (cuuint32_t)nsh,
+                                   which == 0 ? 2u : (cuuint32_t)band_spins};
         CUresult r = encode(which == 0 ? &out->dmap : &out->smap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base,
                             dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -566,17 +643,18 @@ static g4_status make_maps(const void* stg, int n, int es, int nsh, int width, i
     return G4_OK;
 }
 
-static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, int dd, MapPair* out) {
+static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, int dd, int band_spins,
+                          MapPair* out) {
     static std::mutex mu;
-    static std::map<std::tuple<uintptr_t, int, int, int, int>, MapPair> cache;
-    const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(stg), n, nsh, es, dd);
+    static std::map<std::tuple<uintptr_t, int, int, int, int, int>, MapPair> cache;
+    const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(stg), n, nsh, es, dd, band_spins);
     std::lock_guard<std::mutex> lk(mu);
     auto it = cache.find(key);
     if (it != cache.end()) {
         *out = it->second;
         return G4_OK;
     }
-    G4_TRY(make_maps(stg, n, es, nsh, width, dd, out));
+    G4_TRY(make_maps(stg, n, es, nsh, width, dd, band_spins, out));
     if (cache.size() > 4096) cache.clear();
     cache.emplace(key, *out);
     return G4_OK;
@@ -584,6 +662,11 @@ static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, in
 
 template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP>
 static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
+    if constexpr (G::CL > 1) {  // shifted cluster tiles need whole 32-wide strips and CL | chunks
+        const int64_t nx = (prm.hi - prm.lo + G::Q - 1) / G::Q;
+        if (prm.n % 32 != 0 || nx % G::CL != 0)
+            return launch_v2_t<R, RG, typename G::Base, FUSED, MINB, EXP>(prm, st);
+    }
     static bool attr_set = false;
     if (!attr_set) {
         G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
@@ -602,7 +685,8 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
-            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::NSH, G::W, G::DR, &mp));
+            G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::CL > 1 ? G::HS : G::NSH, G::W, G::DR,
+                            G::CL > 1 ? 1 : 2, &mp));
             tp.dmap[i] = mp.dmap;
             tp.smap[i] = mp.smap;
         }
@@ -610,8 +694,25 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
         tp.nx = (int32_t)((planes + G::Q - 1) / G::Q);
         const uint64_t ctas = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
         if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
-        k_accumulate_tma<R, RG, G, FUSED, MINB, EXP><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
-        G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
+        if constexpr (G::CL == 1) {
+            k_accumulate_tma<R, RG, G, FUSED, MINB, EXP><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
+            G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
+        } else {
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)ctas);
+            lc.blockDim = dim3(32 * G::CW);
+            lc.dynamicSmemBytes = G::SMEM;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeClusterDimension;
+            at[0].val.clusterDim.x = G::CL;
+            at[0].val.clusterDim.y = 1;
+            at[0].val.clusterDim.z = 1;
+            lc.attrs = at;
+            lc.numAttrs = 1;
+            G4_TRY(check_cuda(cudaLaunchKernelEx(&lc, k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>, tp),
+                              "k_accumulate_tma cluster launch"));
+        }
     }
     return G4_OK;
 }
@@ -639,6 +740,8 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
 //    8  4x4    4x4      16x16   2   1            17  8x2    2x2      16x4    4   2
 //   11  4x4    4x2      16x8    3   2            19  8x2    1x4       8x8    2   4   (default, P <= 8)
 //                                                20  4x4    2x2       8x8    2   4
+//   21 / 22: geometry 12 in clusters of 4 / 2 (band multicast); 23 / 24: 13 likewise.
+//   Measured slower than 12 / 13 (profiles/r01_summary.md, lab27); selectable only.
 template <typename R, typename RG, bool FUSED>
 static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
     switch (g) {
@@ -665,6 +768,10 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 17: return launch_v2<R, RG, V2Geom<RG, 8, 2, 4, 2, 2>, FUSED, 2>(prm, st);
         case 19: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4>, FUSED, 4>(prm, st);
         case 20: return launch_v2<R, RG, V2Geom<RG, 4, 2, 2, 4, 2>, FUSED, 4>(prm, st);
+        case 21: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2, 1, 4>, FUSED, 2>(prm, st);
+        case 22: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2, 1, 2>, FUSED, 2>(prm, st);
+        case 23: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2, 1, 4>, FUSED, 4>(prm, st);
+        case 24: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2, 1, 2>, FUSED, 4>(prm, st);
         default: return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
     }
 }
@@ -690,6 +797,10 @@ static bool geom_info(int g, GeomInfo* out) {
         case 17: *out = info_of<V2Geom<double, 8, 2, 4, 2, 2>>(2); return true;
         case 19: *out = info_of<V2Geom<double, 8, 1, 2, 2, 4>>(4); return true;
         case 20: *out = info_of<V2Geom<double, 4, 2, 2, 4, 2>>(4); return true;
+        case 21: *out = info_of<V2Geom<double, 8, 2, 3, 4, 2, 1, 4>>(2); return true;
+        case 22: *out = info_of<V2Geom<double, 8, 2, 3, 4, 2, 1, 2>>(2); return true;
+        case 23: *out = info_of<V2Geom<double, 8, 2, 2, 2, 2, 1, 4>>(4); return true;
+        case 24: *out = info_of<V2Geom<double, 8, 2, 2, 2, 2, 1, 2>>(4); return true;
         default: return false;
     }
 }
