@@ -570,19 +570,54 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
                 mbar_wait(&empty[w % NST], (w / NST) & 1);
     }
 
+    // Deferred update, complex128 slices: the warp parks its block in the (now
+    // idle) stage buffers, one 512-B row segment per (p, d), and the TMA engine
+    // adds each segment to the slice (cp.reduce.async.bulk .add.f64): no
+    // per-lane reds (red.global has no 128-bit f64 form, so those cost two
+    // half-sector L2 atomics per entry and stall the LSU queue).
+    constexpr size_t WARP_PARK = (size_t)PP * DD * 32 * sizeof(Cx<R>);
+    if constexpr ((EXP & K1_DEFER) != 0 && sizeof(R) == 8 && PP * DD <= 32 &&
+                  (size_t)NST * G::STAGE_BYTES >= G::CW * WARP_PARK) {
+        __syncthreads();  // every warp is past its last stage read (and every fill has landed)
+        Cx<R>* park = reinterpret_cast<Cx<R>*>(smem_raw + warp * WARP_PARK);
 #pragma unroll
-    for (int p = 0; p < PP; ++p)
-#pragma unroll
-        for (int d = 0; d < DD; ++d)
-            if (okmask & (1u << (p * DD + d))) {
-                if constexpr ((EXP & K1_DEFER) != 0) {
-                    R* a = reinterpret_cast<R*>(gb + p * nn + offg[d]);
-                    atomicAdd(a, acc[p][d].re);
-                    atomicAdd(a + 1, acc[p][d].im);
-                } else if ((EXP & EXP_NOSTORE) == 0 || acc[p][d].re == R(-1234.5)) {
-                    st_g4(gb + p * nn + offg[d], acc[p][d]);
-                }
+        for (int t = 0; t < PP * DD; ++t) park[t * 32 + lane] = acc[t / DD][t % DD];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+        __syncwarp();
+        if (lane < PP * DD) {  // lane t adds block t = (p, d)
+            const int p = lane / DD, d = lane % DD;
+            const int k1 = k1_0 + e0 + d;  // < 2N
+            if (qw + p < P.hi && (CL > 1 || k1 < n)) {
+                const int cnt = CL > 1 ? 32 : min(32, n - j0);  // valid columns j0 + i
+                int k2 = j0 + e0 + d;                             // column of entry 0, < 2N
+                if (k2 >= n) k2 -= n;
+                Cx<R>* row = gb + p * nn + (int64_t)(k1 >= n ? k1 - n : k1) * n;
+                const uint32_t src = smem_u32(park + lane * 32);
+                const int run1 = min(cnt, n - k2);  // up to the row end, then wrap to column 0
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
+                             ::"l"(row + k2), "r"(src), "r"(run1 * 16) : "memory");
+                if (run1 < cnt)
+                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
+                                 ::"l"(row), "r"(src + run1 * 16), "r"((cnt - run1) * 16) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // park read before exit
             }
+        }
+    } else {
+#pragma unroll
+        for (int p = 0; p < PP; ++p)
+#pragma unroll
+            for (int d = 0; d < DD; ++d)
+                if (okmask & (1u << (p * DD + d))) {
+                    if constexpr ((EXP & K1_DEFER) != 0) {
+                        R* a = reinterpret_cast<R*>(gb + p * nn + offg[d]);
+                        atomicAdd(a, acc[p][d].re);
+                        atomicAdd(a + 1, acc[p][d].im);
+                    } else if ((EXP & EXP_NOSTORE) == 0 || acc[p][d].re == R(-1234.5)) {
+                        st_g4(gb + p * nn + offg[d], acc[p][d]);
+                    }
+                }
+    }
 }
 
 // Host: the two sheared tensor maps of one staged payload, cached by (pointer, n, dtype).
@@ -718,10 +753,19 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
 }
 
 // G4_ARITH_FUSED adds the walkers' sum to the slice at the end (K1_DEFER) with
-// >= 4 walkers per pass on >= 16 planes: -9 % time at B = 8 and 16 (lab23).
-// With fewer walkers, or on the small slices of an 8-GPU ring, the L2 atomics
-// cost more than the G4 load they save (r01f: B = 1 and P = 8 lines).
-static bool defer_update(int nbatch, int64_t planes) { return nbatch >= 4 && planes >= 16; }
+// >= 4 walkers per pass.  With the TMA bulk-reduce epilogue (complex128 slices)
+// this pays on any slice height: -2 % at P = 64, B = 8; -19 % at P = 8, B = 8
+// (the 8-GPU ring share); -7 % at N = 4608 (lab28).  With 1-2 walkers the L2
+// read-modify-write costs more than the G4 load it saves (+13 % / +5 %).
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
+}
+static bool defer_update(int nbatch, int64_t planes) {
+    static const int min_w = env_int("G4RING_DEFER_MIN_WALKERS", 4);  // measurement knobs
+    static const int min_p = env_int("G4RING_DEFER_MIN_PLANES", 1);
+    return nbatch >= min_w && planes >= min_p;
+}
 
 template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
 static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {

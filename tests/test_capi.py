@@ -106,7 +106,8 @@ def test_k1_config_host_query():
     _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED))
     try:
         assert cfg(512, 64)[:5] == [2, 8, 4, 16, 8] and cfg(512, 64)[8] == 1   # deferred update, geometry 12
-        assert cfg(512, 64, nbatch=2)[8] == 0 and cfg(512, 8)[8] == 0          # not for B < 4 or P < 16
+        assert cfg(512, 64, nbatch=2)[8] == 0                                  # not for B < 4
+        assert cfg(512, 8)[:5] == [2, 8, 2, 8, 8] and cfg(512, 8)[8] == 1      # 8-GPU share: geometry 19, deferred
     finally:
         _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
     with pytest.raises(errors.ContractViolation):
