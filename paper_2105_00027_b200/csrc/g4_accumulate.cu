@@ -363,9 +363,23 @@ struct alignas(64) TmaParams {
 //   1 = start from zero accumulators (no G4 read)   2 = no G4 write
 //   4 = no shared-memory reads / math  (bits combine; profiles/r01_summary.md)
 // K1_DEFER (production, G4_ARITH_FUSED with >= 4 walkers): the walkers' sum is
-// formed from zero and added to the slice at the end with red.global.add, so
-// no CTA waits on its G4 block (the L2 does the read-modify-write).
-enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, K1_DEFER = 16 };
+// formed from zero and added to the slice at the end -- by TMA bulk reduce for
+// complex128 slices, red.global.add for complex64 -- so no CTA waits on its G4
+// block (the L2 does the read-modify-write).
+// K1_BULKST (production, complex128 slices otherwise): the block is written
+// back by TMA bulk stores from the idle stage buffers.
+enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, K1_DEFER = 16, K1_BULKST = 32 };
+
+// Shared -> global bulk copy by the TMA engine: add (.add.f64 reduction) or store.
+template <bool ADD>
+__device__ __forceinline__ void bulk_out(void* dst, uint32_t src, int bytes) {
+    if constexpr (ADD)
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
+                     ::"l"(dst), "r"(src), "r"(bytes) : "memory");
+    else
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(dst), "r"(src), "r"(bytes) : "memory");
+}
 static int exp_flags() {
     static int e = -1;
     if (e < 0) {
@@ -575,8 +589,12 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     // adds each segment to the slice (cp.reduce.async.bulk .add.f64): no
     // per-lane reds (red.global has no 128-bit f64 form, so those cost two
     // half-sector L2 atomics per entry and stall the LSU queue).
+    // Non-deferred complex128 slices (K1_BULKST): the same park, then a plain
+    // bulk store of each segment: -3 % at B = 1 and 8, -5 % at N = 4608 against
+    // per-lane st.global.cs (lab29).
     constexpr size_t WARP_PARK = (size_t)PP * DD * 32 * sizeof(Cx<R>);
-    if constexpr ((EXP & K1_DEFER) != 0 && sizeof(R) == 8 && PP * DD <= 32 &&
+    constexpr bool DEFER = (EXP & K1_DEFER) != 0;
+    if constexpr ((DEFER || (EXP & K1_BULKST) != 0) && sizeof(R) == 8 && PP * DD <= 32 &&
                   (size_t)NST * G::STAGE_BYTES >= G::CW * WARP_PARK) {
         __syncthreads();  // every warp is past its last stage read (and every fill has landed)
         Cx<R>* park = reinterpret_cast<Cx<R>*>(smem_raw + warp * WARP_PARK);
@@ -594,11 +612,8 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
                 Cx<R>* row = gb + p * nn + (int64_t)(k1 >= n ? k1 - n : k1) * n;
                 const uint32_t src = smem_u32(park + lane * 32);
                 const int run1 = min(cnt, n - k2);  // up to the row end, then wrap to column 0
-                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
-                             ::"l"(row + k2), "r"(src), "r"(run1 * 16) : "memory");
-                if (run1 < cnt)
-                    asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
-                                 ::"l"(row), "r"(src + run1 * 16), "r"((cnt - run1) * 16) : "memory");
+                bulk_out<DEFER>(row + k2, src, run1 * 16);
+                if (run1 < cnt) bulk_out<DEFER>(row, src + run1 * 16, (cnt - run1) * 16);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // park read before exit
             }
@@ -771,6 +786,10 @@ template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
 static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     if constexpr (FUSED && EXP == 0) {
         if (defer_update(prm.nbatch, prm.hi - prm.lo)) return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER>(prm, st);
+    }
+    if constexpr (EXP == 0 && sizeof(R) == 8) {
+        static const bool bulk_store = env_int("G4RING_BULK_STORE", 1) != 0;  // 0: st.global.cs (A/B)
+        if (bulk_store) return launch_v2_t<R, RG, G, FUSED, MINB, K1_BULKST>(prm, st);
     }
     return launch_v2_t<R, RG, G, FUSED, MINB, EXP>(prm, st);
 }
