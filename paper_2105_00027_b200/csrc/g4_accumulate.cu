@@ -370,15 +370,48 @@ struct alignas(64) TmaParams {
 // back by TMA bulk stores from the idle stage buffers.
 enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, K1_DEFER = 16, K1_BULKST = 32 };
 
-// Shared -> global bulk copy by the TMA engine: add (.add.f64 reduction) or store.
-template <bool ADD>
+// Shared -> global bulk copy by the TMA engine: add (.add reduction) or store.
+template <bool ADD, typename R>
 __device__ __forceinline__ void bulk_out(void* dst, uint32_t src, int bytes) {
-    if constexpr (ADD)
+    if constexpr (!ADD)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+                     ::"l"(dst), "r"(src), "r"(bytes) : "memory");
+    else if constexpr (sizeof(R) == 8)
         asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;"
                      ::"l"(dst), "r"(src), "r"(bytes) : "memory");
     else
-        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;"
+        asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;"
                      ::"l"(dst), "r"(src), "r"(bytes) : "memory");
+}
+template <typename R>
+constexpr bool BULK_SLICE = sizeof(R) == 8;  // slices written back by the TMA engine (complex128)
+// One entry through the LSU (segment edges the TMA cannot take).
+template <bool ADD, typename R>
+__device__ __forceinline__ void entry_out(Cx<R>* g, const Cx<R>& v) {
+    if constexpr (ADD) {
+        atomicAdd(&g->re, v.re);
+        atomicAdd(&g->im, v.im);
+    } else {
+        *g = v;
+    }
+}
+// `count` entries from shared `s` to global `g`: bulk where both are 16-B
+// aligned, LSU for an odd head/tail (complex64) or a misaligned pair.
+template <bool ADD, typename R>
+__device__ __forceinline__ void segment_out(Cx<R>* g, const Cx<R>* s, int count) {
+    if (count <= 0) return;
+    if (reinterpret_cast<uintptr_t>(g) & 15) {
+        entry_out<ADD>(g, *s);
+        ++g, ++s, --count;
+    }
+    const uint32_t sa = static_cast<uint32_t>(__cvta_generic_to_shared(s));
+    if (sa & 15) {
+        for (int i = 0; i < count; ++i) entry_out<ADD>(g + i, s[i]);
+        return;
+    }
+    const int m = count & ~(16 / (int)sizeof(Cx<R>) - 1);  // whole 16-B units
+    if (m > 0) bulk_out<ADD, R>(g, sa, m * (int)sizeof(Cx<R>));
+    if (m < count) entry_out<ADD>(g + m, s[m]);
 }
 static int exp_flags() {
     static int e = -1;
@@ -584,36 +617,46 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
                 mbar_wait(&empty[w % NST], (w / NST) & 1);
     }
 
-    // Deferred update, complex128 slices: the warp parks its block in the (now
-    // idle) stage buffers, one 512-B row segment per (p, d), and the TMA engine
-    // adds each segment to the slice (cp.reduce.async.bulk .add.f64): no
-    // per-lane reds (red.global has no 128-bit f64 form, so those cost two
-    // half-sector L2 atomics per entry and stall the LSU queue).
-    // Non-deferred complex128 slices (K1_BULKST): the same park, then a plain
-    // bulk store of each segment: -3 % at B = 1 and 8, -5 % at N = 4608 against
-    // per-lane st.global.cs (lab29).
-    constexpr size_t WARP_PARK = (size_t)PP * DD * 32 * sizeof(Cx<R>);
+    // Deferred update: the warp parks its block in the (now idle) stage buffers,
+    // one row segment per (p, d), and the TMA engine adds each segment to the
+    // slice (cp.reduce.async.bulk .add): no per-lane reds (red.global has no
+    // 128-bit f64 form, so those cost two half-sector L2 atomics per entry and
+    // stall the LSU queue).  Non-deferred (K1_BULKST): the same park, then a
+    // plain bulk store of each segment: -3 % at B = 1 and 8, -5 % at N = 4608
+    // against per-lane st.global.cs (lab29).  Complex64 segments are parked at
+    // the parity of their first column, so that global and shared addresses
+    // agree mod 16 B; an odd head or tail entry goes through the LSU.  That is
+    // slower than per-lane reds/stores for their 256-B segments (lab30: +8 %
+    // fused, +4-7 % exact), so complex64 slices keep the LSU path (BULK_SLICE).
+    constexpr int PSTR = sizeof(R) == 8 ? 32 : 34;  // parked entries per (p, d) segment
+    constexpr size_t WARP_PARK = (size_t)PP * DD * PSTR * sizeof(Cx<R>);
     constexpr bool DEFER = (EXP & K1_DEFER) != 0;
-    if constexpr ((DEFER || (EXP & K1_BULKST) != 0) && sizeof(R) == 8 && PP * DD <= 32 &&
+    if constexpr ((DEFER || (EXP & K1_BULKST) != 0) && PP * DD <= 32 && BULK_SLICE<R> &&
                   (size_t)NST * G::STAGE_BYTES >= G::CW * WARP_PARK) {
         __syncthreads();  // every warp is past its last stage read (and every fill has landed)
         Cx<R>* park = reinterpret_cast<Cx<R>*>(smem_raw + warp * WARP_PARK);
 #pragma unroll
-        for (int t = 0; t < PP * DD; ++t) park[t * 32 + lane] = acc[t / DD][t % DD];
+        for (int d = 0; d < DD; ++d) {
+            int k2 = j0 + e0 + d;  // column of the segment's entry 0, < 2N
+            if (k2 >= n) k2 -= n;
+            const int sh = sizeof(R) == 8 ? 0 : (k2 & 1);
+#pragma unroll
+            for (int p = 0; p < PP; ++p) park[(p * DD + d) * PSTR + sh + lane] = acc[p][d];
+        }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
         __syncwarp();
-        if (lane < PP * DD) {  // lane t adds block t = (p, d)
+        if (lane < PP * DD) {  // lane t writes segment t = (p, d)
             const int p = lane / DD, d = lane % DD;
             const int k1 = k1_0 + e0 + d;  // < 2N
             if (qw + p < P.hi && (CL > 1 || k1 < n)) {
                 const int cnt = CL > 1 ? 32 : min(32, n - j0);  // valid columns j0 + i
-                int k2 = j0 + e0 + d;                             // column of entry 0, < 2N
+                int k2 = j0 + e0 + d;
                 if (k2 >= n) k2 -= n;
                 Cx<R>* row = gb + p * nn + (int64_t)(k1 >= n ? k1 - n : k1) * n;
-                const uint32_t src = smem_u32(park + lane * 32);
+                const Cx<R>* seg = park + lane * PSTR + (sizeof(R) == 8 ? 0 : (k2 & 1));
                 const int run1 = min(cnt, n - k2);  // up to the row end, then wrap to column 0
-                bulk_out<DEFER>(row + k2, src, run1 * 16);
-                if (run1 < cnt) bulk_out<DEFER>(row, src + run1 * 16, (cnt - run1) * 16);
+                segment_out<DEFER>(row + k2, seg, run1);
+                if (run1 < cnt) segment_out<DEFER>(row, seg + run1, cnt - run1);
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // park read before exit
             }
@@ -787,7 +830,7 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     if constexpr (FUSED && EXP == 0) {
         if (defer_update(prm.nbatch, prm.hi - prm.lo)) return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER>(prm, st);
     }
-    if constexpr (EXP == 0 && sizeof(R) == 8) {
+    if constexpr (EXP == 0 && BULK_SLICE<R>) {
         static const bool bulk_store = env_int("G4RING_BULK_STORE", 1) != 0;  // 0: st.global.cs (A/B)
         if (bulk_store) return launch_v2_t<R, RG, G, FUSED, MINB, K1_BULKST>(prm, st);
     }
