@@ -351,6 +351,8 @@ template <typename R>
 struct alignas(64) TmaParams {
     CUtensorMap dmap[TMA_MAXW];  // direct tiles: sheared map, 4-row boxes
     CUtensorMap smap[TMA_MAXW];  // shifted bands: sheared map, NSH-row boxes
+    CUtensorMap gmap;            // the slice, sheared: (x, k1, plane) -> G4[plane][k1][k1 + x - N]
+    int32_t use_gmap;            // gmap encoded (complex128 slices)
     Cx<R>* g4;
     int64_t lo, hi;
     int32_t n;
@@ -412,6 +414,10 @@ __device__ __forceinline__ void segment_out(Cx<R>* g, const Cx<R>* s, int count)
     const int m = count & ~(16 / (int)sizeof(Cx<R>) - 1);  // whole 16-B units
     if (m > 0) bulk_out<ADD, R>(g, sa, m * (int)sizeof(Cx<R>));
     if (m < count) entry_out<ADD>(g + m, s[m]);
+}
+static int env_int(const char* name, int dflt) {
+    const char* v = getenv(name);
+    return v ? atoi(v) : dflt;
 }
 static int exp_flags() {
     static int e = -1;
@@ -645,7 +651,25 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
         __syncwarp();
-        if (lane < PP * DD) {  // lane t writes segment t = (p, d)
+        // Interior blocks (no row or column wrap, all planes in the slice): the
+        // whole PP x DD x 32 block is one sheared box of the slice's tensor map.
+        const bool interior = P.use_gmap && qw + PP <= P.hi && k1_0 + e0 + DD - 1 < n &&
+                              j0 + 31 + e0 + DD - 1 < n;
+        if (interior) {
+            if (lane == 0) {
+                const int c0 = 2 * (j0 - k1_0 + n), c1 = k1_0 + e0, c2 = (int)(qw - P.lo);
+                if constexpr (DEFER)
+                    asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+                                 " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&P.gmap)),
+                                 "r"(smem_u32(park)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+                else
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.tile.bulk_group"
+                                 " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&P.gmap)),
+                                 "r"(smem_u32(park)), "r"(c0), "r"(c1), "r"(c2) : "memory");
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+            }
+        } else if (lane < PP * DD) {  // lane t writes segment t = (p, d)
             const int p = lane / DD, d = lane % DD;
             const int k1 = k1_0 + e0 + d;  // < 2N
             if (qw + p < P.hi && (CL > 1 || k1 < n)) {
@@ -753,6 +777,43 @@ static g4_status get_maps(const void* stg, int n, int es, int nsh, int width, in
     return G4_OK;
 }
 
+// Sheared tensor map of a complex128 slice for the K1 write-back: element
+// (x, r, p) (x in doubles) is G4[p][r][r + x/2 - N], i.e. dim-1 stride (N+1)
+// entries, so a box of DD rows is a K3-diagonal strip.  The base lies N
+// entries before the slice; only interior boxes (no column wrap) are used.
+static bool g4_gmap_enabled() {
+    static const bool on = env_int("G4RING_GMAP", 1) != 0;  // 0: per-segment bulk ops (A/B)
+    return on;
+}
+static g4_status slice_map(const void* g4, int n, int64_t planes, int pp, int dd, CUtensorMap* out) {
+    static std::mutex mu;
+    static std::map<std::tuple<uintptr_t, int, int64_t, int, int>, CUtensorMap> cache;
+    const auto key = std::make_tuple(reinterpret_cast<uintptr_t>(g4), n, planes, pp, dd);
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return G4_OK;
+    }
+    PFN_encodeTiled encode = tensor_map_encoder();
+    if (!encode) return fail(G4_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    const cuuint64_t dims[3] = {(cuuint64_t)4 * n, (cuuint64_t)n, (cuuint64_t)planes};
+    const cuuint64_t strides[2] = {(cuuint64_t)(n + 1) * 16, (cuuint64_t)n * n * 16};
+    const cuuint32_t box[3] = {64, (cuuint32_t)dd, (cuuint32_t)pp};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    void* base = static_cast<char*>(const_cast<void*>(g4)) - (size_t)n * 16;
+    CUresult r = encode(out, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, base, dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                        CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled (slice) failed: %d", (int)r);
+        return G4_ERR_CUDA;
+    }
+    if (cache.size() > 1024) cache.clear();
+    cache.emplace(key, *out);
+    return G4_OK;
+}
+
 template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP>
 static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     if constexpr (G::CL > 1) {  // shifted cluster tiles need whole 32-wide strips and CL | chunks
@@ -775,6 +836,10 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
         tp.hi = prm.hi;
         tp.n = n;
         tp.off = sheared_offset(n, G::ES);
+        if constexpr (BULK_SLICE<R> && G::PP * G::DD <= 32) {
+            G4_TRY(slice_map(prm.g4, n, prm.hi - prm.lo, G::PP, G::DD, &tp.gmap));
+            tp.use_gmap = g4_gmap_enabled() ? 1 : 0;
+        }
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
@@ -815,10 +880,6 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
 // this pays on any slice height: -2 % at P = 64, B = 8; -19 % at P = 8, B = 8
 // (the 8-GPU ring share); -7 % at N = 4608 (lab28).  With 1-2 walkers the L2
 // read-modify-write costs more than the G4 load it saves (+13 % / +5 %).
-static int env_int(const char* name, int dflt) {
-    const char* v = getenv(name);
-    return v ? atoi(v) : dflt;
-}
 static bool defer_update(int nbatch, int64_t planes) {
     static const int min_w = env_int("G4RING_DEFER_MIN_WALKERS", 4);  // measurement knobs
     static const int min_p = env_int("G4RING_DEFER_MIN_PLANES", 1);
