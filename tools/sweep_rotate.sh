@@ -1,4 +1,5 @@
-# producer refill duty rotating over the warps (G4RING_ROTATE=1) vs lane 0 of warp 0
+# producer refill duty rotating over the warps (G4RING_ROTATE=1) vs lane 0 of warp 0.
+# Record of lab33 only: the knob was removed after this measurement (no gain).
 cd $GRAFT_REPO_ROOT
 G4RING_ROTATE=1 timeout 300 python tools/cluster_check.py | grep -c " ok$"
 L="timeout 120 python tools/k1_lab.py"
