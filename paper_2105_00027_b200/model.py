@@ -235,8 +235,8 @@ class K1Calibration:
     sms: int = 148
     fp64_instr_per_s: float = 17.0e12  # DFMA issue
     fp32_instr_per_s: float = 35.7e12  # FFMA issue
-    eff_hbm: float = 0.72              # B = 1: 0.708 of HBM
-    eff_smem: float = 0.74             # B = 8 / 16: 0.69 / 0.80 of the smem data path
+    eff_hbm: float = 0.86              # B = 1: 0.84-0.88 of HBM (r01j; 0.71 in r01c)
+    eff_smem: float = 0.78             # exact, N = 512: B = 8 / 16 at 0.72 / 0.88 of the smem data path (r01j)
     eff_fp: float = 0.85
     launch_s: float = 4e-6             # launch + tail of one pass
 
@@ -281,6 +281,11 @@ def k1_pass_time(n: int, planes: int, batch: int, dtype: str = "c128", arith: st
     bounds = {"hbm": hbm_b / (cal.hbm_gbs * 1e9 * cal.eff_hbm),
               "smem": smem_b / (cal.smem_bytes_per_s * cal.eff_smem * util),
               "fp": fp_i / (fpeak * cal.eff_fp * util)}
+    if g["deferred"]:
+        # The deferred update's L2 read-modify-write and the payload fills share
+        # the L2 <-> SM path and do not overlap: the r01j fused lines (B = 8, 16;
+        # N = 512 and 4608) sit within 7 % of the SUM of the two times at peak.
+        bounds["hbm+smem"] = hbm_b / (cal.hbm_gbs * 1e9) + smem_b / (cal.smem_bytes_per_s * util)
     bound = max(bounds, key=bounds.get)
     t = bounds[bound] + cal.launch_s
     return {"time_s": t, "bound": bound, "bounds_s": bounds, "updates": upd, "hbm_bytes": hbm_b,
