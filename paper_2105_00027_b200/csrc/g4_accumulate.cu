@@ -370,7 +370,7 @@ struct alignas(64) TmaParams {
 // block (the L2 does the read-modify-write).
 // K1_BULKST (production, complex128 slices otherwise): the block is written
 // back by TMA bulk stores from the idle stage buffers.
-enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, K1_DEFER = 16, K1_BULKST = 32 };
+enum : int { EXP_NOLOAD = 1, EXP_NOSTORE = 2, EXP_NOMATH = 4, K1_DEFER = 16, K1_BULKST = 32, EXP_SCALAR_RED = 64 };
 
 // Shared -> global bulk copy by the TMA engine: add (.add reduction) or store.
 template <bool ADD, typename R>
@@ -691,7 +691,11 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
 #pragma unroll
             for (int d = 0; d < DD; ++d)
                 if (okmask & (1u << (p * DD + d))) {
-                    if constexpr ((EXP & K1_DEFER) != 0) {
+                    if constexpr ((EXP & K1_DEFER) != 0 && sizeof(R) == 4 && (EXP & EXP_SCALAR_RED) == 0) {
+                        // one 8-B vector red per complex64 entry (a warp covers 256 B)
+                        asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(gb + p * nn + offg[d]),
+                                     "f"(acc[p][d].re), "f"(acc[p][d].im) : "memory");
+                    } else if constexpr ((EXP & K1_DEFER) != 0) {
                         R* a = reinterpret_cast<R*>(gb + p * nn + offg[d]);
                         atomicAdd(a, acc[p][d].re);
                         atomicAdd(a + 1, acc[p][d].im);
@@ -889,7 +893,13 @@ static bool defer_update(int nbatch, int64_t planes) {
 template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
 static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
     if constexpr (FUSED && EXP == 0) {
-        if (defer_update(prm.nbatch, prm.hi - prm.lo)) return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER>(prm, st);
+        if (defer_update(prm.nbatch, prm.hi - prm.lo)) {
+            if constexpr (sizeof(R) == 4) {  // A/B knob: scalar f32 reds instead of one v2 red per entry
+                static const bool scalar = env_int("G4RING_SCALAR_RED", 0) != 0;
+                if (scalar) return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER | EXP_SCALAR_RED>(prm, st);
+            }
+            return launch_v2_t<R, RG, G, FUSED, MINB, K1_DEFER>(prm, st);
+        }
     }
     if constexpr (EXP == 0 && BULK_SLICE<R>) {
         static const bool bulk_store = env_int("G4RING_BULK_STORE", 1) != 0;  // 0: st.global.cs (A/B)
