@@ -31,8 +31,11 @@
 //    stride LD+1 elements) that turn diagonals into rectangular boxes.  The halo
 //    of the staged layout means no box ever wraps.  Consumers wait on the
 //    stage's mbarrier, read their elements from shared memory (contiguous per
-//    warp: conflict-free) and release the stage.  Geometry choice and the
-//    measured alternatives: launch_v2_geom below, DESIGN.md section 4.
+//    warp: conflict-free) and release the stage.  After the last walker the
+//    idle stage buffers take each warp's block, and the TMA engine writes it
+//    back (complex128): one box of a sheared tensor map of the slice per warp,
+//    stored (exact) or added in L2 (fused, deferred update).  Geometry choice
+//    and the measured alternatives: launch_v2_geom below, DESIGN.md section 4.
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
