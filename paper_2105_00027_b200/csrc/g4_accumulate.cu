@@ -50,7 +50,7 @@
 
 namespace g4 {
 
-// Kernel selection: 0 = auto (v2 for complex128 with N >= 64, else v1),
+// Kernel selection: 0 = auto (v2 for N >= 64 and >= 4 planes, any dtype; else v1),
 // 1 = v1 everywhere, 2 = v2 wherever it applies.  G4RING_KERNEL overrides.
 static int g_variant = -1;
 static int kernel_variant() {
