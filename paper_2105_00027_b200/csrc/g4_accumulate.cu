@@ -317,13 +317,22 @@ constexpr int TMA_MAXW = 32;  // walkers per launch (2 tensor maps each, kernel 
 // (k1 - q, k2 - q), so all CL CTAs need the SAME band: each loads HS = NSH / CL
 // of its rows and multicasts them to the whole cluster (TMA .multicast::cluster),
 // cutting the L2 -> SM band traffic by CL.  Needs N % 32 == 0 and chunks % CL == 0.
-template <typename R, int PP_, int CW_, int NST_, int DD_ = 4, int CWR_ = 1, int PF_ = 1, int CL_ = 1>
+//
+// PW = 1: warp specialisation.  The CW = 4 consumer warps form warp group 0;
+// warp group 1 (4 warps) only produces: thread 128 issues every refill as soon
+// as its stage is released.  setmaxnreg moves the registers: the producer
+// group drops to 24, the consumer group rises to 232 (launch: 128 x 256).
+template <typename R, int PP_, int CW_, int NST_, int DD_ = 4, int CWR_ = 1, int PF_ = 1, int CL_ = 1,
+          int PW_ = 0>
 struct V2Geom {
     static constexpr int PP = PP_, DD = DD_, CWQ = CW_, CWR = CWR_, NST = NST_;
     static constexpr int PF = PF_;  // shifted operands loaded this many diagonals ahead
     static constexpr int CL = CL_;  // CTAs per cluster (band multicast)
-    using Base = V2Geom<R, PP_, CW_, NST_, DD_, CWR_, PF_, 1>;
-    static constexpr int CW = CWQ * CWR;                          // warps per CTA
+    static constexpr int PW = PW_;  // 1: a producer warp group
+    using Base = V2Geom<R, PP_, CW_, NST_, DD_, CWR_, PF_, 1, PW_>;
+    static constexpr int CW = CWQ * CWR;                          // consumer warps per CTA
+    static constexpr int THREADS = 32 * CW + 128 * PW;
+    static_assert(PW == 0 || (CW == 4 && CL == 1), "producer warp group: 4 consumer warps, no clusters");
     static constexpr int Q = PP * CWQ, DR = DD * CWR;             // CTA tile: planes x diagonal entries
     static constexpr int ES = sizeof(Cx<R>);                      // bytes per complex entry
     static constexpr int NSH = Q + DR - 1;                        // shifted row segments (band height)
@@ -455,7 +464,7 @@ __device__ __forceinline__ Stg<float> lds_plain(const Cx<float>* u, const Cx<flo
 }
 
 template <typename R, typename RG, class G, bool FUSED, int MINB, int EXP = 0>
-__global__ void __launch_bounds__(32 * G::CW, MINB)
+__global__ void __launch_bounds__(G::THREADS, MINB)
 k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     constexpr int PP = G::PP, DD = G::DD, NST = G::NST;
     constexpr int EW = G::ES / 8;  // 64-bit TMA elements per complex entry
@@ -473,7 +482,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     const int crank = CL > 1 ? tc.x % CL : 0;
     const int j0 = CL > 1 ? wrap(tc.y * 32 + crank * Q, n) : tc.y * 32;
     const int k1_0 = CL > 1 ? wrap(tc.z * DR + crank * Q, n) : tc.z * DR;
-    const bool producer = threadIdx.x == 0;
+    const bool producer = threadIdx.x == (G::PW ? 128 : 0);
     // Sheared coordinates (c1, c2) address stg[c2][c1 - off + c2].
     //  direct tile: rows k1_0 + i, columns j0 + i + j      -> (j0 - k1_0 + off, k1_0)
     //  shifted band: rows R0 + i, columns C0 + i + j with
@@ -499,6 +508,11 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     };
     // A warp is done with stage s: release it in every CTA that multicasts into it.
     auto release = [&](int s) {
+        // The stage's last operands are read by ld.shared right before this
+        // point and may still be in flight (the math that consumes them can be
+        // scheduled after the arrive): order every lane's generic-proxy reads
+        // before the async-proxy (TMA) refill the arrive allows.
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if constexpr (CL == 1) {
             if (lane == 0) mbar_arrive(&empty[s]);
@@ -522,6 +536,25 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         cluster_sync_relaxed();
         if (producer)
             for (int w = 0; w < NST && w < P.nbatch; ++w) issue(w);
+    }
+    constexpr int PSTR = sizeof(R) == 8 ? 32 : 34;  // parked entries per (p, d) segment (epilogue)
+    constexpr size_t WARP_PARK = (size_t)PP * DD * PSTR * sizeof(Cx<R>);
+    constexpr bool DEFER = (EXP & K1_DEFER) != 0;
+    constexpr bool PARK = (DEFER || (EXP & K1_BULKST) != 0) && PP * DD <= 32 && BULK_SLICE<R> &&
+                          (size_t)NST * G::STAGE_BYTES >= G::CW * WARP_PARK;
+    if constexpr (G::PW == 1) {
+        if (warp >= 4) {  // producer warp group
+            asm volatile("setmaxnreg.dec.sync.aligned.u32 24;" ::: "memory");
+            if (producer)
+                for (int w = NST; w < P.nbatch; ++w) {
+                    const int wp = w - NST;
+                    mbar_wait(&empty[wp % NST], (wp / NST) & 1);
+                    issue(w);
+                }
+            __syncwarp();
+            return;  // the epilogue's barrier is among the consumer warps only
+        }
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
     }
 
     // ---- warp (wq, wr) owns planes q0 + PP*wq + p and diagonal entries e = DD*wr + d ----
@@ -567,7 +600,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
         const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
         const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
         if constexpr ((EXP & EXP_NOMATH) != 0) {
-            if (producer && w >= 1 && w - 1 + NST < P.nbatch) {
+            if (G::PW == 0 && producer && w >= 1 && w - 1 + NST < P.nbatch) {
                 mbar_wait(&empty[(w - 1) % NST], ((w - 1) / NST) & 1);
                 issue(w - 1 + NST);
             }
@@ -587,7 +620,7 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
             sbuf[i] = widen<R>(lds_plain(sh_u + sh_o + i * G::W, sh_d + sh_o + i * G::W));
         // Producer duty (lane 0 of warp 0): refill the stage every warp released in
         // the previous iteration with walker w - 1 + NST; its TMA overlaps this math.
-        if (producer && w >= 1 && w - 1 + NST < P.nbatch) {
+        if (G::PW == 0 && producer && w >= 1 && w - 1 + NST < P.nbatch) {
             const int wp = w - 1;
             mbar_wait(&empty[wp % NST], (wp / NST) & 1);
             issue(wp + NST);
@@ -637,12 +670,12 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     // agree mod 16 B; an odd head or tail entry goes through the LSU.  That is
     // slower than per-lane reds/stores for their 256-B segments (lab30: +8 %
     // fused, +4-7 % exact), so complex64 slices keep the LSU path (BULK_SLICE).
-    constexpr int PSTR = sizeof(R) == 8 ? 32 : 34;  // parked entries per (p, d) segment
-    constexpr size_t WARP_PARK = (size_t)PP * DD * PSTR * sizeof(Cx<R>);
-    constexpr bool DEFER = (EXP & K1_DEFER) != 0;
-    if constexpr ((DEFER || (EXP & K1_BULKST) != 0) && PP * DD <= 32 && BULK_SLICE<R> &&
-                  (size_t)NST * G::STAGE_BYTES >= G::CW * WARP_PARK) {
-        __syncthreads();  // every warp is past its last stage read (and every fill has landed)
+    if constexpr (PARK) {
+        // every consumer warp is past its last stage read (and every fill has landed)
+        if constexpr (G::PW == 1)
+            asm volatile("barrier.sync 1, %0;" ::"r"(32 * G::CW) : "memory");
+        else
+            __syncthreads();
         Cx<R>* park = reinterpret_cast<Cx<R>*>(smem_raw + warp * WARP_PARK);
 #pragma unroll
         for (int d = 0; d < DD; ++d) {
@@ -860,12 +893,12 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
         const uint64_t ctas = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
         if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
         if constexpr (G::CL == 1) {
-            k_accumulate_tma<R, RG, G, FUSED, MINB, EXP><<<(unsigned)ctas, 32 * G::CW, G::SMEM, st>>>(tp);
+            k_accumulate_tma<R, RG, G, FUSED, MINB, EXP><<<(unsigned)ctas, G::THREADS, G::SMEM, st>>>(tp);
             G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
         } else {
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3((unsigned)ctas);
-            lc.blockDim = dim3(32 * G::CW);
+            lc.blockDim = dim3(G::THREADS);
             lc.dynamicSmemBytes = G::SMEM;
             lc.stream = st;
             cudaLaunchAttribute at[1];
@@ -914,7 +947,7 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
 // v2 geometries: PP x DD thread block, CWQ x CWR warps (CTA tile Q x DR), NST
 // stages, CTAs per SM.  Sweep results: profiles/r01_summary.md.
 //   id  PPxDD  CWQxCWR  QxDR   NST CTA/SM       id  PPxDD  CWQxCWR  QxDR   NST CTA/SM
-//    0  4x4    4x1      16x4    3   3            12  8x4    2x2      16x8    3   2   (default, P >= 16, fused)
+//    0  4x4    4x1      16x4    3   3            12  8x4    2x2      16x8    3   2
 //    3  4x4    4x1      16x4    2   4            13  8x2    2x2      16x4    2   4   (default, P >= 16, exact)
 //    7  4x4    4x2      16x8    2   2            16  4x4    4x1      16x4    4   2
 //    8  4x4    4x4      16x16   2   1            17  8x2    2x2      16x4    4   2
@@ -922,6 +955,8 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
 //                                                20  4x4    2x2       8x8    2   4
 //   21 / 22: geometry 12 in clusters of 4 / 2 (band multicast); 23 / 24: 13 likewise.
 //   Measured slower than 12 / 13 (profiles/r01_summary.md, lab27); selectable only.
+//   25: geometry 12 plus a producer warp group (setmaxnreg 24 / 232): the fused
+//   default for P >= 16 (-4 % at B = 8 and 16, lab35).
 template <typename R, typename RG, bool FUSED>
 static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
     switch (g) {
@@ -952,6 +987,7 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 22: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2, 1, 2>, FUSED, 2>(prm, st);
         case 23: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2, 1, 4>, FUSED, 4>(prm, st);
         case 24: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2, 1, 2>, FUSED, 4>(prm, st);
+        case 25: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2, 1, 1, 1>, FUSED, 2>(prm, st);
         default: return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
     }
 }
@@ -981,6 +1017,7 @@ static bool geom_info(int g, GeomInfo* out) {
         case 22: *out = info_of<V2Geom<double, 8, 2, 3, 4, 2, 1, 2>>(2); return true;
         case 23: *out = info_of<V2Geom<double, 8, 2, 2, 2, 2, 1, 4>>(4); return true;
         case 24: *out = info_of<V2Geom<double, 8, 2, 2, 2, 2, 1, 2>>(4); return true;
+        case 25: *out = info_of<V2Geom<double, 8, 2, 3, 4, 2, 1, 1, 1>>(2); return true;
         default: return false;
     }
 }
@@ -990,7 +1027,7 @@ static bool geom_info(int g, GeomInfo* out) {
 // not read at CTA start (K1_DEFER), the 2-CTA/SM, 32-entry-register-block
 // geometry 12 beats 13 (lab24: -7 % at B = 16, -10 % at N = 4608).
 // G4RING_V2GEOM overrides.
-static int v2_geom(int64_t planes, bool deferred) {
+static int v2_geom(int64_t planes, bool deferred, bool c64_slice) {
     static int forced = -2;
     if (forced == -2) {
         const char* e = getenv("G4RING_V2GEOM");
@@ -998,7 +1035,8 @@ static int v2_geom(int64_t planes, bool deferred) {
     }
     if (forced >= 0) return forced;
     if (planes < 16) return 19;
-    return deferred ? 12 : 13;
+    if (!deferred) return 13;
+    return c64_slice ? 12 : 25;  // the producer warp group loses on complex64 slices (+15 %, lab35)
 }
 
 static bool use_v2(int n, int64_t planes) {
@@ -1010,7 +1048,8 @@ template <typename R, typename RG, bool FUSED>
 static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     if (use_v2(prm.n, planes))
-        return launch_v2_geom<R, RG, FUSED>(v2_geom(planes, FUSED && defer_update(prm.nbatch, planes)), prm, st);
+        return launch_v2_geom<R, RG, FUSED>(
+            v2_geom(planes, FUSED && defer_update(prm.nbatch, planes), sizeof(R) == 4), prm, st);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
@@ -1092,7 +1131,8 @@ g4_status g4_k1_config(int32_t n, int64_t planes, int32_t nbatch, int32_t dtype,
     if (use_v2(n, planes)) {
         const bool deferred = g_arith == G4_ARITH_FUSED && defer_update(walkers, planes);
         GeomInfo gi;
-        if (!geom_info(v2_geom(planes, deferred), &gi)) return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
+        if (!geom_info(v2_geom(planes, deferred, dtype == G4_C64), &gi))
+            return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
         const int32_t v[9] = {2, gi.pp, gi.dd, gi.q, gi.dr, gi.nst, gi.ctas, gi.warps, deferred ? 1 : 0};
         std::memcpy(out, v, sizeof(v));
     } else {

@@ -1,4 +1,4 @@
-# warp-specialised K1: geometry 25 = geometry 12 + a producer warp group (setmaxnreg 24/232) (lab35)
+# warp-specialised K1: geometry 25 = geometry 12 + a producer warp group (setmaxnreg 24/232) (lab35; now the fused default)
 cd $GRAFT_REPO_ROOT
 G4RING_V2GEOM=25 timeout 300 python tools/cluster_check.py | grep -c " ok$"
 L="timeout 120 python tools/k1_lab.py"
