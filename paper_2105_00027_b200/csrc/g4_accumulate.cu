@@ -554,7 +554,12 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
             __syncwarp();
             return;  // the epilogue's barrier is among the consumer warps only
         }
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 232;" ::: "memory");
+        // launch budget L = 65536 / (MINB x THREADS) registers (8-aligned); the
+        // producer group's 24 go to the consumers: 128 (24 + C) = THREADS x L.
+        constexpr int L = (65536 / (MINB * G::THREADS)) / 8 * 8;
+        constexpr int C = (2 * L - 24) > 232 ? 232 : (2 * L - 24) / 8 * 8;
+        static_assert(C >= 128, "producer warp group leaves the consumers too few registers");
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C) : "memory");
     }
 
     // ---- warp (wq, wr) owns planes q0 + PP*wq + p and diagonal entries e = DD*wr + d ----
@@ -956,7 +961,9 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
 //   21 / 22: geometry 12 in clusters of 4 / 2 (band multicast); 23 / 24: 13 likewise.
 //   Measured slower than 12 / 13 (profiles/r01_summary.md, lab27); selectable only.
 //   25: geometry 12 plus a producer warp group (setmaxnreg 24 / 232): the fused
-//   default for P >= 16 (-4 % at B = 8 and 16, lab35).
+//   default for P >= 16 (-4 % at B = 8 and 16, lab35).  27: geometry 19 likewise
+//   (3 CTAs/SM, consumers at 136): within 2 % of 19 at P = 8, B = 8 (lab36);
+//   selectable only.
 template <typename R, typename RG, bool FUSED>
 static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
     switch (g) {
@@ -988,6 +995,7 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 23: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2, 1, 4>, FUSED, 4>(prm, st);
         case 24: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2, 1, 2>, FUSED, 4>(prm, st);
         case 25: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2, 1, 1, 1>, FUSED, 2>(prm, st);
+        case 27: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4, 1, 1, 1>, FUSED, 3>(prm, st);
         default: return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
     }
 }
@@ -1018,6 +1026,7 @@ static bool geom_info(int g, GeomInfo* out) {
         case 23: *out = info_of<V2Geom<double, 8, 2, 2, 2, 2, 1, 4>>(4); return true;
         case 24: *out = info_of<V2Geom<double, 8, 2, 2, 2, 2, 1, 2>>(4); return true;
         case 25: *out = info_of<V2Geom<double, 8, 2, 3, 4, 2, 1, 1, 1>>(2); return true;
+        case 27: *out = info_of<V2Geom<double, 8, 1, 2, 2, 4, 1, 1, 1>>(3); return true;
         default: return false;
     }
 }
