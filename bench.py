@@ -47,6 +47,44 @@ CONFIGS = {
 SINGLE_GPU_PLANES = {"c4": 72}
 
 
+def workload(args):
+    """(n_k, n_w, planes, description) of the run: BASELINE config `--config`;
+    config 4 on one GPU is its per-GPU share of the 8-GPU ring."""
+    n_k, n_w, planes, desc = CONFIGS[args.config]
+    if args.gpus == 1 and args.config in SINGLE_GPU_PLANES:
+        planes = SINGLE_GPU_PLANES[args.config]
+        desc += f" -- per-GPU share on one GPU: {planes} planes"
+    if args.gpus == 1 and args.planes:
+        planes = args.planes
+    return n_k, n_w, planes, desc
+
+
+def ring_shape(args, n_ranks):
+    """Sub-ring size S and lanes of an N > 1 run (config 3: 2 sub-rings of 4, 2 lanes)."""
+    S = args.subring_size or (min(4, n_ranks) if args.config == "c3" else n_ranks)
+    lanes = args.lanes or (2 if args.config == "c3" else 1)
+    return S, lanes
+
+
+def workload_config(args, n_ranks):
+    """The JSON `config` object -- identical in both arms (ours and --impl
+    reference) for the same flags and N, so the driver can match them."""
+    n_k, n_w, planes, desc = workload(args)
+    n = n_k * n_w
+    eb = 8 if args.dtype == "c64" else 16
+    if n_ranks == 1:
+        return {"workload": f"{args.config}: {desc}", "n": n, "planes": planes, "walkers_per_pass": args.batch,
+                "subring_size": 1, "lanes": 1,
+                "l2": ("slice larger than L2 (no flush needed)" if planes * n * n * eb > 126e6
+                       else "slice fits L2 (L2-resident caveat)")}
+    from oracle import oracle as O
+    S, lanes = ring_shape(args, n_ranks)
+    p_local = max(hi - lo for lo, hi in O.partition(planes, S))
+    return {"workload": f"{args.config}: {desc}", "n": n, "planes": planes, "planes_per_gpu": p_local,
+            "walkers_per_rank_per_step": args.batch, "subring_size": S, "lanes": lanes,
+            "parallelism": f"{n_ranks // S} sub-ring(s) of {S}"}
+
+
 def measured_peaks():
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -185,9 +223,12 @@ def run_reference(args):
     if rank != 0:
         return
     from oracle import oracle as O
-    n_k, n_w, planes, desc = CONFIGS[args.config]
+    n_k, n_w, planes, desc = workload(args)
     n = n_k * n_w
     cores = O.cpu_count()
+    n_ranks = int(os.environ.get("WORLD_SIZE", "1"))
+    # a bounded sample of the workload per step (B walkers over all planes); updates/s is a
+    # per-update rate, so the sample is the same at every N (the CPU does not scale with N)
     walkers = args.batch
     rate, step_s, used = cpu_throughput(n, planes, walkers, args.steps, args.warmup, cores)
     line = {
@@ -195,8 +236,7 @@ def run_reference(args):
         "n_gpus": args.gpus, "device": "cpu (all host cores; the same work at every N)", "steps": args.steps, "warmup": args.warmup, "ms_per_step": step_s * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128",
         "data": "synthetic (reference generator, float mode, seed 0)",
-        "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
-                   "walkers_per_step": walkers},
+        "config": workload_config(args, n_ranks),
         "cpu_baseline": {"value": rate, "unit": "updates/s", "cores": used, "kind": "port",
                          "sample": f"{walkers} walkers x {planes} planes x N^2={n * n} per step, "
                                    f"numpy port of accumulate_g4 in {used} processes on disjoint "
@@ -232,12 +272,7 @@ def run_gpu(args):
 
     lib = _lib.load()
     _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if args.arith == "fused" else _lib.G4_ARITH_EXACT))
-    n_k, n_w, planes, desc = CONFIGS[args.config]
-    if args.config in SINGLE_GPU_PLANES:
-        planes = SINGLE_GPU_PLANES[args.config]
-        desc += f" -- per-GPU share on one GPU: {planes} planes"
-    if args.planes:
-        planes = args.planes
+    n_k, n_w, planes, desc = workload(args)
     sp = T.CombinedIndexSpace(n_k, n_w)
     n = sp.size
     dtype = torch.complex64 if args.dtype == "c64" else torch.complex128    # G4 slice
@@ -287,6 +322,8 @@ def run_gpu(args):
 
     # -- e2e: reference-layout payloads in pinned host memory through g4_accumulate --
     e2e = run_e2e(args, lib, T, sp, planes, dtype, eb, dev)
+    # -- the timed kernel's output, checked after timing (sampled planes vs the C oracle) --
+    parity = parity_check(T, sl, pools[0], planes, n, dtype, args.arith)
 
     line = {
         "metric": "G4 updates/s", "value": value, "unit": "updates/s", "n_gpus": 1,
@@ -295,10 +332,7 @@ def run_gpu(args):
         "parity": ("bitwise vs the reference" if args.arith == "exact"
                    else "within 1e-10 relative (north_star; tests 1e-12), integer payloads bitwise"),
         "data": "synthetic (reference counter-based generator on device, float mode, seed 0)",
-        "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
-                   "walkers_per_pass": B, "subring_size": 1, "lanes": 1,
-                   "l2": "slice larger than L2 (no flush needed)" if planes * n * n * eb > 126e6
-                   else "slice fits L2 (L2-resident caveat)"},
+        "config": workload_config(args, 1),
         "hbm_gbs": achieved,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": k1_traffic(lib, n, planes, B, args.dtype, args.arith),
@@ -307,6 +341,7 @@ def run_gpu(args):
         "onchip": onchip_bounds(lib, n, planes, args.dtype, args.arith, B, upd_step / (statistics.mean(k_ms) * 1e-3)),
         "clocks": clk.summary(),
         "e2e": e2e,
+        "parity_check": parity,
         "gpu_launches": args.steps,
         "batch_sweep": batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B),
         "other_arith": other_arith_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B,
@@ -324,6 +359,36 @@ def run_gpu(args):
                       f"numpy port of accumulate_g4 in {used} processes on disjoint K3 ranges; "
                       f"host {cpu_model()}"}
     print(json.dumps(line), flush=True)
+
+
+def parity_check(T, sl, walkers, planes, n, dtype, arith, sample=(0, None, -1)):
+    """One more pass of the timed launch configuration, from a zeroed slice
+    with the first walker pool, then sampled planes (first, middle, last)
+    against the C oracle (test infrastructure, used here only as the checker,
+    after the timed region).  Bitwise expected in exact mode; fused mode is
+    judged against 1e-12 relative (complex64 slices: 1e-5)."""
+    import numpy as np
+    import torch
+    from oracle import oracle as O
+    sl.data.zero_()
+    T.accumulate_g4_batch(sl, walkers)
+    torch.cuda.synchronize()
+    qs = sorted({q if q is not None and q >= 0 else (planes // 2 if q is None else planes + q) for q in sample})
+    host = [(g.up.contiguous().cpu().numpy().astype(np.complex128),
+             g.down.contiguous().cpu().numpy().astype(np.complex128)) for g in walkers]
+    worst, bitwise = 0.0, True
+    for q in qs:
+        got = sl.data[q].cpu().numpy().astype(np.complex128)
+        ref = np.zeros((1, n, n), np.complex128)
+        for up, down in host:
+            O.accumulate(ref, q, q + 1, up, down)
+        if dtype == torch.complex64:
+            ref = ref.astype(np.complex64).astype(np.complex128)
+        bitwise &= bool(np.array_equal(got, ref[0]))
+        worst = max(worst, float(np.abs(got - ref[0]).max() / max(np.abs(ref).max(), 1e-300)))
+    tol = 1e-5 if dtype == torch.complex64 else (0.0 if arith == "exact" else 1e-12)
+    return {"planes": qs, "walkers": len(walkers), "max_rel_err": worst, "bitwise": bitwise, "tol": tol,
+            "ok": bool(worst <= tol), "checker": "oracle/g4_oracle.c (C restatement of tensor.py:233-251)"}
 
 
 def k1_traffic(lib, n, planes, B, dtype, arith):
@@ -596,11 +661,10 @@ def run_ring(args):
     _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if args.arith == "fused" else _lib.G4_ARITH_EXACT))
     world = E.Control()
     rank, n_ranks = world.rank, world.size
-    n_k, n_w, planes, desc = CONFIGS[args.config]
+    n_k, n_w, planes, desc = workload(args)
     B = args.batch
     # BASELINE config 3 is 8 GPUs as 2 sub-rings of 4 with 2 walker streams (lanes) per GPU
-    S = args.subring_size or (min(4, n_ranks) if args.config == "c3" else n_ranks)
-    lanes = args.lanes or (2 if args.config == "c3" else 1)
+    S, lanes = ring_shape(args, n_ranks)
     cfg = E.ExperimentConfig(n_k=n_k, n_w=n_w, world_size=n_ranks, subring_size=S, lanes=lanes,
                              measurements=B, seed=0, value_mode="float", planes=planes, batch=B,
                              dtype=args.dtype, gather=False, instrument=False, timeout_s=120.0)
@@ -660,10 +724,9 @@ def run_ring(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": args.dtype, "arith": args.arith,
         "data": "synthetic (reference counter-based generator on device, float mode, seed 0; resident)",
-        "config": {"workload": f"{args.config}: {desc}", "n": n, "planes": planes,
-                   "planes_per_gpu": p_local, "walkers_per_rank_per_step": B, "subring_size": S,
-                   "lanes": lanes, "parallelism": f"{n_ranks // S} sub-ring(s) of {S}",
-                   "devices": torch.cuda.device_count()},
+        "config": workload_config(args, n_ranks),
+        "devices": {"visible": torch.cuda.device_count(), "ranks": n_ranks,
+                    "ranks_per_device": -(-n_ranks // max(torch.cuda.device_count(), 1))},
         "per_gpu_updates_per_s": value / n_ranks,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                      "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,

@@ -45,6 +45,7 @@ from .tensor import (CombinedIndexSpace, GtSlice, Origin, _dtype_code, accumulat
                      make_partition, staged_shape)
 
 VALUE_MODES = ("float", "integer")
+ARITH_MODES = {"exact": _lib.G4_ARITH_EXACT, "fused": _lib.G4_ARITH_FUSED}
 _MODE_CODE = {"float": _lib.G4_MODE_FLOAT, "integer": _lib.G4_MODE_INTEGER}
 
 
@@ -70,6 +71,8 @@ class ExperimentConfig:
     dtype: str = "c128"            # "c128" (reference), "c64", or "c128g64" (c128 G4, c64 payloads)
     gather: bool = True            # assemble the full tensor on world rank 0
     sample_planes: tuple[int, ...] = ()  # K3 planes copied to world rank 0 (report.samples)
+    arith: str = "exact"           # K1 arithmetic: "exact" (bitwise reference order) or "fused" (FMA
+                                   # chains + deferred update, within 1e-12; g4_set_arith_mode)
     # test hooks (never part of a user config, as in the reference)
     ring_steps_override: int | None = None
     fault: str | None = None
@@ -111,6 +114,8 @@ def validate_config(cfg: ExperimentConfig) -> None:
         raise ConfigError(f"dtype must be c128, c64 or c128g64, got {cfg.dtype!r}")
     if cfg.timeout_s <= 0:
         raise ConfigError("timeout_s must be positive")
+    if cfg.arith not in ARITH_MODES:
+        raise ConfigError(f"arith must be one of {tuple(ARITH_MODES)}, got {cfg.arith!r}")
 
 
 # ---------------------------------------------------------------------------
@@ -669,6 +674,15 @@ def rank_main(cfg: ExperimentConfig, world: Control | None = None) -> Experiment
     r = world.rank
     device = device_for_rank(r)
     torch.cuda.set_device(device)
+    lib = _lib.load()
+    _lib.check(lib.g4_set_arith_mode(ARITH_MODES[cfg.arith]), "set_arith_mode")
+    try:
+        return _rank_main(cfg, world, r, device)
+    finally:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT), "set_arith_mode")
+
+
+def _rank_main(cfg: ExperimentConfig, world: Control, r: int, device: torch.device) -> ExperimentReport | None:
     torch.cuda.reset_peak_memory_stats(device)
     sub = build_subrings(world, cfg.subring_size)
     pos_group = world.split(r % cfg.subring_size, r // cfg.subring_size)  # same position across sub-rings

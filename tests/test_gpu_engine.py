@@ -202,3 +202,35 @@ def test_verify_harness_like_reference():
     res = A.verify(c, runs=2)
     assert res.passed and len(res.reports) == 2 and res.mean("l2_real") < 1e-12
     assert not A.verify(c, runs=1, corrupt=True).passed
+
+
+@pytest.mark.parametrize("kw", [
+    dict(value_mode="integer"),
+    dict(value_mode="float"),
+    dict(value_mode="float", dtype="c128g64"),
+    dict(value_mode="float", dtype="c64"),
+    dict(value_mode="integer", world_size=4, subring_size=2),               # 2 sub-rings + reduce
+    dict(value_mode="float", direction="alternate", lanes=2),
+])
+def test_fused_ring_multi_plane_share(kw):
+    """The ring in G4_ARITH_FUSED (the bench's arithmetic) with >= 16 planes per
+    rank and >= 4 payloads per K1 pass, so every pass runs the deferred
+    multi-plane kernel.  Integer payloads bitwise; float within 1e-12
+    (c128), 1e-6 L1/L2 (c64-rounded payloads) and 1e-5 (c64 slices)."""
+    base = dict(n_k=4, n_w=16, world_size=2, subring_size=2, lanes=1, measurements=8, batch=4, planes=64,
+                arith="fused", instrument=False, seed=21)
+    base.update(kw)
+    c = cfg(**base)
+    rep = E.run_experiment(c)
+    ref = oracle_of(c)
+    got = rep.tensor.astype(np.complex128)
+    if c.value_mode == "integer":
+        assert np.array_equal(got, ref)
+    elif c.dtype == "c128":
+        np.testing.assert_allclose(got, ref, rtol=1e-12, atol=1e-12 * np.abs(ref).max())
+    else:
+        r = O.compare(ref, got)
+        assert max(r["l1_real"], r["l1_imag"], r["l2_real"], r["l2_imag"]) < (1e-6 if c.dtype == "c128g64"
+                                                                                 else 1e-5)
+    for rr in range(c.world_size):
+        assert rep.meas_counts[rr] == c.subring_size * c.measurements * c.lanes

@@ -439,14 +439,14 @@ def test_bench_workload_full_slice(oracle, cuda_dev):
 def test_cluster_multicast_geometry_parity():
     """Geometry 22 (geometry 12 in 2-CTA clusters sharing the shifted band by TMA
     multicast; selectable, not a default) against the C oracle: exact bitwise,
-    fused within 1e-12, including the N % 32 != 0 fallback (tools/cluster_check.py)."""
+    fused within 1e-12, including the N % 32 != 0 fallback (tools/geom_check.py)."""
     import os
     import subprocess
     import sys
     from pathlib import Path
     root = Path(__file__).resolve().parent.parent
     env = dict(os.environ, G4RING_V2GEOM="22")
-    r = subprocess.run([sys.executable, str(root / "tools" / "cluster_check.py")], env=env, cwd=root,
+    r = subprocess.run([sys.executable, str(root / "tools" / "geom_check.py")], env=env, cwd=root,
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(" ok") == 24

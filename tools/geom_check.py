@@ -1,15 +1,18 @@
 #!/usr/bin/env python
 """Parity of one forced K1 geometry (G4RING_V2GEOM in the environment) against
-the C oracle on small slices, exact and fused arithmetic.  Used to check the
-cluster-multicast geometries (21-24) before they are timed:
+the C oracle, exact and fused arithmetic, on small slices and on the bench's
+own N = 512 x 64-plane x 8-walker shape:
 
-    G4RING_V2GEOM=21 python tools/cluster_check.py
+    G4RING_V2GEOM=25 python tools/geom_check.py [--repeat 3]
 
-Prints one line per case and exits 1 on any mismatch.  Measurement tool; the
-tests in tests/ cover the production geometries.
+Prints one line per case and exits 1 on any mismatch.  Run by
+tests/test_gpu_headline.py (production and warp-specialised geometries,
+repeated to catch timing-dependent races) and tests/test_gpu_kernels.py
+(cluster geometry 22).
 """
 from __future__ import annotations
 
+import argparse
 import sys
 from pathlib import Path
 
@@ -33,10 +36,13 @@ CASES = [  # n, lo, hi, walkers, payload dtype
 
 
 def main() -> int:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--repeat", type=int, default=1)
+    args = ap.parse_args()
     lib = _lib.load()
     dev = torch.device("cuda", 0)
     bad = 0
-    for arith in ("exact", "fused"):
+    for arith in [a for _ in range(args.repeat) for a in ("exact", "fused")]:
         _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if arith == "fused" else _lib.G4_ARITH_EXACT))
         for n, lo, hi, nb, dt in CASES:
             sp = T.CombinedIndexSpace(1, n)
@@ -64,6 +70,7 @@ def main() -> int:
                 bad += not ok
                 print(f"{arith:5s} n={n} [{lo},{hi}) B={nb} {dt:5s} {mode:7s} max_rel_err={err:.2e} "
                       f"{'ok' if ok else 'MISMATCH'}", flush=True)
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
     return 1 if bad else 0
 
 
