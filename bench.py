@@ -473,7 +473,7 @@ def onchip_bounds(lib, n, planes, dtype, arith, B, upd_per_s):
     peb = 16 if dtype == "c128" else 8        # payload entry
     lds = 2 * peb * (pp + 2 * dd - 1) / (pp * dd)            # operand loads per update
     width = 32 if peb == 16 else 34
-    fill = 2 * peb * width * (dr + q + dr - 1) / (q * dr * 32) if variant == 2 else 0.0  # TMA writes
+    fill = 2 * peb * width * (dr + q + dr - 1) / (q * dr * 32) if variant >= 2 else 0.0  # TMA writes
     g4 = 0.0 if deferred else 2 * eb / B                     # G4 block in and out through L1 (deferred: L2 reduction)
     path = lds + fill + g4
     props = torch.cuda.get_device_properties(torch.cuda.current_device())

@@ -19,7 +19,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libg4ring.so"
-SOURCES = ["g4_util.cpp", "g4_accumulate.cu", "g4_prep.cu", "g4_ring.cu", "g4_ring_driver.cu"]
+SOURCES = ["g4_util.cpp", "g4_accumulate.cu", "g4_accumulate_pst.cu", "g4_prep.cu", "g4_ring.cu", "g4_ring_driver.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -43,9 +43,9 @@ def build(verbose: bool = False, force: bool = False) -> Path:
         return LIB
     out_dir = PKG / "build"
     out_dir.mkdir(exist_ok=True)
-    objs = []
     common = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", str(ROOT / "include")]
-    for src in SOURCES:
+
+    def compile_one(src: str) -> str:
         obj = out_dir / (src.rsplit(".", 1)[0] + ".o")
         cmd = [nvcc(), *ARCH, *common, "-lineinfo", "-fmad=false", "-c", str(CSRC / src), "-o", str(obj)]
         if verbose and src.endswith(".cu"):
@@ -56,7 +56,12 @@ def build(verbose: bool = False, force: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose:
             sys.stderr.write(res.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    # the translation units are independent: compile them concurrently
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+        objs = list(ex.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [nvcc(), *ARCH, "-shared", "-o", str(tmp), *objs, "-lpthread"]
     res = subprocess.run(cmd, capture_output=True, text=True)

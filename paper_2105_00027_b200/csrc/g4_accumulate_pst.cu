@@ -1,0 +1,424 @@
+// g4_accumulate_pst.cu -- K1 v3: the persistent, warp-specialised fused update
+// of a complex128 slice with a tensor-memory hand-off (replaces, like v2,
+// ringacc/tensor.py:233-251; G4_ARITH_FUSED with the deferred update).
+//
+// One CTA per SM loops over CTA tiles (Q planes x DR diagonal entries x 32
+// columns; the tile order is v2's L2-aware tile_coord, CTA c taking tiles c,
+// c + grid, ...).  Four warp groups:
+//   WG0-1 consumers (8 warps, 216 registers): each owns a PP x DD register
+//     block per tile (v2's block and op sequence: update_fused over the walkers
+//     in order, from zero accumulators).  After the tile's last walker the
+//     block goes to tensor memory (tcgen05.st, 128 columns per warp, two
+//     buffers) and the warp starts the next tile at once.
+//   WG2 epilogue (4 warps, 56 registers): warp 8 + q drains TMEM lane quarter
+//     q (tcgen05.ld) for the two consumer warps that own it, parks each
+//     (plane, 4-diagonal) chunk of 2 KB in shared memory and adds it to the
+//     slice in L2 with one TMA tensor reduce (sheared slice map, box 32 x 4 x 1)
+//     -- the deferred update of v2, now off the consumers' critical path.
+//   WG3 producer (1 active lane, 24 registers): streams both TMA boxes of every
+//     walker of every tile into an NST-stage ring, running ahead across tile
+//     boundaries (no pipeline drain or refill between tiles).
+// What this removes against v2 (geometry 25, one 4-warp tile per CTA, 4096
+// CTAs): the per-CTA prologue (barrier init, first fills landing) and epilogue
+// (park + bulk reduce + waiting for it to read) on every tile, and one of the
+// two CTAs per SM sitting in them; and the CTA tile doubles (8 consumer warps),
+// cutting the TMA fill bytes per update from 7.75 to 5.9 B.
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+
+#include "g4_k1.cuh"
+
+namespace g4 {
+
+// Geometry: PP x DD thread block, CWQ x CWR consumer warps (CW = 8), NST
+// stages of both boxes, NPARK 2-KB park slots per epilogue warp.
+template <typename RG, int PP_, int DD_, int CWQ_, int CWR_, int NST_, int NPARK_>
+struct V3Geom {
+    static constexpr int PP = PP_, DD = DD_, CWQ = CWQ_, CWR = CWR_, NST = NST_, NPARK = NPARK_;
+    static constexpr int CW = CWQ * CWR;
+    static_assert(CW == 8, "two consumer warp groups");
+    static constexpr int THREADS = 512;                      // 4 warp groups
+    static constexpr int Q = PP * CWQ, DR = DD * CWR;       // CTA tile: planes x diagonal entries
+    static constexpr int ES = sizeof(Cx<RG>);               // payload entry bytes
+    static constexpr int NSH = Q + DR - 1;                  // shifted band rows
+    static constexpr int W = ES == 8 ? 34 : 32;             // box row width (entries), see V2Geom
+    static constexpr int DIR_ELEMS = DR * W, SH_ELEMS = NSH * W;
+    static constexpr uint32_t DIR_BYTES = 2 * DIR_ELEMS * ES;
+    static constexpr uint32_t SH_BYTES = 2 * SH_ELEMS * ES;
+    static constexpr uint32_t DIR_OFF = 0;
+    static constexpr uint32_t SH_OFF = (DIR_BYTES + 127) / 128 * 128;
+    static constexpr uint32_t STAGE_BYTES = (SH_OFF + SH_BYTES + 127) / 128 * 128;
+    static constexpr uint32_t CHUNK_BYTES = DD * 32 * 16;   // one (plane, DD diagonals) chunk of the slice
+    static constexpr uint32_t PARK_OFF = NST * STAGE_BYTES;
+    static constexpr uint32_t PARK_BYTES = 4 * NPARK * CHUNK_BYTES;
+    static constexpr uint32_t BAR_OFF = PARK_OFF + PARK_BYTES;
+    static constexpr size_t SMEM = BAR_OFF + (2 * NST + 4) * sizeof(uint64_t) + 16;
+    static constexpr int BLOCK_COLS = PP * DD * 4;          // TMEM columns per consumer warp block
+    static_assert(2 * 2 * BLOCK_COLS <= 512, "two buffers x two consumer warps per lane quarter");
+    static_assert(SMEM <= 227 * 1024, "v3 stages + park exceed shared memory");
+    static_assert(NPARK % 2 == 0 && NPARK >= 4, "park slots hold chunk pairs");
+    static_assert(PP % 2 == 0, "the epilogue drains chunk pairs");
+    static_assert(NSH <= G4_HALO_ROWS && NSH + W + 1 < G4_HALO_COLS && DR + W <= G4_HALO_COLS,
+                  "halo too small for the v3 boxes");
+};
+
+// Register budget of the four warp groups (setmaxnreg): 2 x 128 x 216 +
+// 128 x 56 + 128 x 24 = 65536 (the epilogue holds a 32-register TMEM load;
+// the consumers fit 216 without spills).
+constexpr int V3_REG_CONSUMER = 216, V3_REG_EPILOGUE = 56, V3_REG_PRODUCER = 24;
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
+        "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};"
+        ::"r"(taddr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+        "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]),
+        "r"(v[16]), "r"(v[17]), "r"(v[18]), "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]),
+        "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]), "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr)
+        : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, "
+        "%14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+          "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]),
+          "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]),
+          "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr)
+        : "memory");
+}
+// A parked chunk (DD row segments of 32 entries, slice plane `plane`, rows k1b + d,
+// columns k2b + d + i for the valid columns j0 + i < N) added segment by segment:
+// rows past N skipped, columns split at the row end.  Edge tiles only (one lane).
+// Inlined: an ABI call from a setmaxnreg-reduced warp group may use registers the
+// group no longer owns (a __noinline__ version corrupted the edge chunks).
+__device__ __forceinline__ void pst_edge_chunk(const TmaParams<double>& P, int plane, int k1b, int k2b, int j0, int dd,
+                                            const Cx<double>* park) {
+    const int n = P.n;
+    Cx<double>* base = P.g4 + (int64_t)plane * n * n;
+    const int cnt = min(32, n - j0);
+    for (int d = 0; d < dd; ++d) {
+        const int k1 = k1b + d;  // < 2N
+        if (k1 >= n) break;
+        int k2 = k2b + d;
+        if (k2 >= n) k2 -= n;
+        Cx<double>* row = base + (int64_t)k1 * n;
+        const int run1 = min(cnt, n - k2);
+        segment_out<true, double>(row + k2, park + d * 32, run1);
+        if (run1 < cnt) segment_out<true, double>(row, park + d * 32 + run1, cnt - run1);
+    }
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// Per-tile geometry shared by the three roles.
+struct V3Tile {
+    int64_t q0;
+    int k1_0, j0;
+};
+template <class G>
+__device__ __forceinline__ V3Tile v3_tile(const TmaParams<double>& P, int lin) {
+    const int n = P.n;
+    const TileCoord tc = tile_coord((unsigned)lin, P.nx, (n + 31) / 32, (n + G::DR - 1) / G::DR);
+    return {P.lo + (int64_t)tc.x * G::Q, tc.z * G::DR, tc.y * 32};
+}
+
+template <typename RG, class G>
+__global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant__ TmaParams<double> P) {
+    using R = double;
+    constexpr int PP = G::PP, DD = G::DD, NST = G::NST, DR = G::DR;
+    constexpr int EW = G::ES / 8;  // 64-bit TMA elements per payload entry
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + G::BAR_OFF);
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;  // [2] consumers -> epilogue: the tile's blocks are in TMEM buffer b
+    uint64_t* tready = tfull + 2;   // [2] epilogue -> consumers: TMEM buffer b has been drained
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 2);
+
+    const int n = P.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = P.nx * ((n + 31) / 32) * ((n + DR - 1) / DR);
+    const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int nb = P.nbatch;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], G::CW);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull[b], G::CW);
+            mbar_init(&tready[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 8) {  // the whole of TMEM (one CTA per SM)
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp >= 12) {
+        // ---------------- producer ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_PRODUCER) : "memory");
+        if (threadIdx.x == 384) {
+            int it = 0;
+            for (int k = 0; k < my_tiles; ++k) {
+                const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
+                const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
+                const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
+                const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
+                const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;
+                for (int w = 0; w < nb; ++w, ++it) {
+                    const int s = it % NST;
+                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
+                    unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
+                    tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s]);
+                    tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
+                }
+            }
+        }
+        __syncwarp();
+        return;
+    }
+
+    if (warp >= 8) {
+        // ---------------- epilogue ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_EPILOGUE) : "memory");
+        const int q = warp - 8;  // TMEM lane quarter (and consumer warps q, q + 4)
+        // park: NPARK slots of a chunk PAIR (2 x 2 KB) per epilogue warp
+        const uint32_t park0 = smem_u32(smem_raw + G::PARK_OFF) + (uint32_t)q * G::NPARK * G::CHUNK_BYTES +
+                               lane * (uint32_t)sizeof(Cx<R>);
+        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+        const uint64_t gmap = reinterpret_cast<uint64_t>(&P.gmap);
+        int pair = 0;  // chunk pairs parked by this warp (slot = pair % NSLOT)
+        constexpr int NSLOT = G::NPARK / 2;
+        for (int k = 0; k < my_tiles; ++k) {
+            const int b = k & 1;
+            mbar_wait(&tfull[b], (k >> 1) & 1);
+            tc_fence_after();
+            const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
+                const int p_lo = (int)(t.q0 - P.lo) + PP * wq;  // slice-relative plane of p = 0
+                const int e0 = DD * wr;
+                const int k1b = t.k1_0 + e0;  // row of diagonal 0 (< 2N)
+                const bool box = P.use_gmap && k1b + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n;
+                const int c0 = 2 * (t.j0 - t.k1_0 + n);
+                const int np = min(PP, (int)(P.hi - P.lo) - p_lo);  // planes of the block inside the slice
+                const uint32_t tb = tq + b * 256 + h * G::BLOCK_COLS;
+#pragma unroll 1
+                for (int p = 0; p < np; p += 2) {
+                    uint32_t v[32];
+                    tmem_ld32(tb + p * 16, v);
+                    tmem_wait_ld();
+                    const uint32_t slot = park0 + (uint32_t)(pair % NSLOT) * 2 * G::CHUNK_BYTES;
+                    if (pair >= NSLOT) {  // the slot's previous reduces have read it
+                        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NSLOT - 1) : "memory");
+                        __syncwarp();
+                    }
+#pragma unroll
+                    for (int i = 0; i < 2 * DD; ++i)  // chunk i / DD, diagonal i % DD, this lane's column
+                        asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(slot + i * 32 * 16),
+                                     "r"(v[4 * i]), "r"(v[4 * i + 1]), "r"(v[4 * i + 2]), "r"(v[4 * i + 3]) : "memory");
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+                    __syncwarp();
+                    if (lane == 0) {
+                        const uint32_t sp = slot - lane * (uint32_t)sizeof(Cx<R>);
+                        for (int c = 0; c < 2 && p + c < np; ++c) {
+                            if (box)  // one sheared box of the slice map: 32 entries x DD diagonals x 1 plane
+                                asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+                                             " [%0, {%2, %3, %4}], [%1];" ::"l"(gmap), "r"(sp + c * G::CHUNK_BYTES),
+                                             "r"(c0), "r"(k1b), "r"(p_lo + p + c) : "memory");
+                            else
+                                pst_edge_chunk(P, p_lo + p + c, k1b, t.j0 + e0, t.j0, DD,
+                                               reinterpret_cast<const Cx<double>*>(smem_raw + (sp + c * G::CHUNK_BYTES -
+                                                                                               smem_u32(smem_raw))));
+                        }
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                    ++pair;
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tready[b]);
+        }
+        if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        __syncwarp();
+        // every epilogue warp is past its last tcgen05.ld: release TMEM
+        asm volatile("barrier.sync 1, 128;" ::: "memory");
+        if (warp == 8) {
+            tc_fence_after();
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(V3_REG_CONSUMER) : "memory");
+    const int wq = warp % G::CWQ, wr = warp / G::CWQ;
+    const int e0 = DD * wr;
+    const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (warp >> 2) * G::BLOCK_COLS;
+    int it = 0;
+    for (int k = 0; k < my_tiles; ++k) {
+        const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
+        int ps = 0, pd = 0;
+        if constexpr (G::ES == 8) {
+            const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
+            const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
+            pd = (t.j0 - t.k1_0 + P.off) & 1;
+            ps = (C0 - R0 + P.off) & 1;
+        }
+        const int sh_o = (PP * wq + DR - DD - e0) * G::W + (31 - lane) + ps;  // band row of (p, d): + j * W
+        const int dr_o = e0 * G::W + lane + pd;                                // direct row d: + d * W
+        Cx<R> acc[PP][DD];
+#pragma unroll
+        for (int p = 0; p < PP; ++p)
+#pragma unroll
+            for (int d = 0; d < DD; ++d) acc[p][d].re = acc[p][d].im = R(0);
+#pragma unroll 1
+        for (int w = 0; w < nb; ++w, ++it) {
+            const int s = it % NST;
+            mbar_wait(&full[s], (it / NST) & 1);
+            const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
+            const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
+            const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
+            const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
+            Stg<R> dv[DD];
+#pragma unroll
+            for (int d = 0; d < DD; ++d) dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
+            constexpr int NJ = PP + DD - 1;  // diagonals p - d
+            Stg<R> S = widen<R>(lds_plain(sh_u + sh_o, sh_d + sh_o));
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                Stg<R> Sn;
+                if (j + 1 < NJ) Sn = widen<R>(lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W));
+#pragma unroll
+                for (int d = 0; d < DD; ++d) {
+                    const int p = j + d - (DD - 1);
+                    if (p < 0 || p >= PP) continue;
+                    update_fused(acc[p][d], S, dv[d]);
+                }
+                if (j + 1 < NJ) S = Sn;
+            }
+            // release the stage once its values are consumed (see v2: the refill is
+            // an async-proxy write, the last ld.shared may still be in flight)
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        // hand the block to the epilogue through TMEM buffer b
+        const int b = k & 1;
+        if (k >= 2) mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < PP * DD / 8; ++c) {  // 8 entries (32 columns) per store
+            uint32_t v[32];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const Cx<R>& a = acc[(8 * c + i) / DD][(8 * c + i) % DD];
+                v[4 * i + 0] = (uint32_t)__double2loint(a.re);
+                v[4 * i + 1] = (uint32_t)__double2hiint(a.re);
+                v[4 * i + 2] = (uint32_t)__double2loint(a.im);
+                v[4 * i + 3] = (uint32_t)__double2hiint(a.im);
+            }
+            tmem_st32(tq + b * 256 + c * 32, v);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tfull[b]);
+    }
+}
+
+template <typename RG, class G>
+static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                              int32_t nbatch, cudaStream_t st) {
+    auto kern = k_accumulate_pst<RG, G>;
+    int dev = 0;
+    G4_CUDA(cudaGetDevice(&dev));
+    {  // the >48 KB shared-memory opt-in is per device
+        static std::mutex mu;
+        static uint64_t done = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(done & (1ull << (dev & 63)))) {
+            G4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+            done |= 1ull << (dev & 63);
+        }
+    }
+    int sms = 0;
+    G4_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    for (int b0 = 0; b0 < nbatch; b0 += TMA_MAXW) {
+        TmaParams<double> tp;
+        std::memset(&tp, 0, sizeof(tp));
+        tp.g4 = static_cast<Cx<double>*>(g4p);
+        tp.lo = lo;
+        tp.hi = hi;
+        tp.n = n;
+        tp.off = sheared_offset(n, G::ES);
+        G4_TRY(slice_map(g4p, n, hi - lo, 1, G::DD, &tp.gmap));
+        tp.use_gmap = g4_gmap_enabled() ? 1 : 0;
+        tp.nbatch = std::min(TMA_MAXW, nbatch - b0);
+        for (int i = 0; i < tp.nbatch; ++i) {
+            MapPair mp;
+            G4_TRY(get_maps(staged[b0 + i], n, G::ES, G::NSH, G::W, G::DR, 2, &mp));
+            tp.dmap[i] = mp.dmap;
+            tp.smap[i] = mp.smap;
+        }
+        tp.nx = (int32_t)((hi - lo + G::Q - 1) / G::Q);
+        const int64_t tiles = (int64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
+        if (tiles >= (1ll << 31)) return fail(G4_ERR_CONTRACT, "accumulate: tile count too large");
+        const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+        kern<<<grid, G::THREADS, G::SMEM, st>>>(tp);
+        G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_pst launch"));
+    }
+    return G4_OK;
+}
+
+// v3 geometries (id >= 40 in the G4RING_V2GEOM numbering):
+//   40: 8x4 blocks, 2x4 warps (tile 16 planes x 16 diagonals), 4 stages, 4 park slots
+//   (a 32 x 8 tile, 4x2 warps, needs a band of 39 rows + 32 columns: beyond the staged halo)
+//   42: as 40 with 3 stages and 8 park slots
+template <typename RG>
+g4_status launch_pst(int geom, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                     int32_t nbatch, cudaStream_t st) {
+    switch (geom) {
+        case 40: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 4, 4>>(g4p, lo, hi, n, staged, nbatch, st);
+        case 42: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 3, 8>>(g4p, lo, hi, n, staged, nbatch, st);
+        default: return fail(G4_ERR_CONTRACT, "unknown v3 geometry");
+    }
+}
+template g4_status launch_pst<double>(int, void*, int64_t, int64_t, int32_t, const void* const*, int32_t,
+                                      cudaStream_t);
+template g4_status launch_pst<float>(int, void*, int64_t, int64_t, int32_t, const void* const*, int32_t,
+                                     cudaStream_t);
+
+bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst) {
+    switch (geom) {
+        case 40: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 4; return true;
+        case 42: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 3; return true;
+        default: return false;
+    }
+}
+
+}  // namespace g4

@@ -270,7 +270,7 @@ def k1_pass_time(n: int, planes: int, batch: int, dtype: str = "c128", arith: st
     hbm_b = 2 * planes * n * n * eb + batch * 2 * n * n * peb
     lds = 2 * peb * (g["pp"] + 2 * g["dd"] - 1) / (g["pp"] * g["dd"])
     width = 32 if peb == 16 else 34
-    fill = 2 * peb * width * (g["dr"] + g["q"] + g["dr"] - 1) / (g["q"] * g["dr"] * 32) if g["variant"] == 2 else 0.0
+    fill = 2 * peb * width * (g["dr"] + g["q"] + g["dr"] - 1) / (g["q"] * g["dr"] * 32) if g["variant"] >= 2 else 0.0
     smem_b = upd * (lds + fill + (0.0 if g["deferred"] else 2 * eb / batch))
     fp_i = upd * (8 if arith == "fused" else 12)
     fpeak = cal.fp32_instr_per_s if dtype == "c64" else cal.fp64_instr_per_s

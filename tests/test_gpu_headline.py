@@ -1,9 +1,9 @@
 """Parity of the paths the bench headline and the BASELINE configs actually run,
 at their own shapes ("Next round" item 1).  GPU only.
 
-* the fused default (G4_ARITH_FUSED: deferred update, TMA bulk-reduce
-  epilogue) on the full N = 512 x 64-plane x B = 8 bench workload, on a zero
-  and on a nonzero slice;
+* the fused default (G4_ARITH_FUSED: the persistent K1 v3 with its TMEM
+  hand-off and TMA tensor-reduce epilogue) on the full N = 512 x 64-plane x
+  B = 8 bench workload, on a zero and on a nonzero slice;
 * config 4's per-GPU share (N = 4608, 72 planes) through the multi-plane
   kernel, exact and fused, sampled planes of ONE 72-plane slice;
 * config 3's index space (N = 1024, n_k = 16, n_w = 64), 16 planes;
@@ -68,7 +68,7 @@ def test_headline_fused_full_slice(oracle, cuda_dev, fused, start):
     sp = T.CombinedIndexSpace(16, 32)
     n, planes, B = sp.size, 64, 8
     cfg = k1_config(n, planes, B)
-    assert cfg[0] == 2 and cfg[8] == 1, f"headline is not the deferred multi-plane kernel: {cfg}"
+    assert cfg[0] == 3 and cfg[8] == 1, f"headline is not the persistent deferred kernel (v3): {cfg}"
     rng = np.random.default_rng(7)
     for mode in ("integer", "float"):
         if start == "zero":
@@ -110,7 +110,7 @@ def test_config4_share_sampled_planes(oracle, cuda_dev, arith):
     try:
         sp = T.CombinedIndexSpace(36, 128)
         n, lo, hi, B = sp.size, 144, 216, 4
-        assert k1_config(n, hi - lo, B)[0] == 2
+        assert k1_config(n, hi - lo, B)[0] == (3 if arith == "fused" else 2)
         gs = _walkers(sp, 3, "float", B, dev=cuda_dev)
         sl = T.GtSlice.zeros(sp, lo, hi, device=cuda_dev)
         T.accumulate_g4_batch(sl, gs)
@@ -241,7 +241,7 @@ def test_reference_layout_entry_rejects_small_workspace(cuda_dev):
     assert type(e.value).__name__ == "ContractViolation"
 
 
-@pytest.mark.parametrize("geom", ["25", "27", "12", "13", "19"])
+@pytest.mark.parametrize("geom", ["40", "25", "27", "12", "13", "19"])
 def test_forced_geometry_parity_repeated(geom):
     """Each production (and selectable warp-specialised) geometry forced on the
     small-slice suite AND the full N = 512 x 64 x 8 bench shape, exact and
