@@ -26,6 +26,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <vector>
 
 #include "g4_k1.cuh"
 
@@ -55,6 +56,8 @@ struct V3Geom {
     static constexpr uint32_t BAR_OFF = PARK_OFF + PARK_BYTES;
     static constexpr size_t SMEM = BAR_OFF + (2 * NST + 4) * sizeof(uint64_t) + 16;
     static constexpr int BLOCK_COLS = PP * DD * 4;          // TMEM columns per consumer warp block
+    // the last tile's blocks (CW x PP chunks) fit the idle stage buffers: consumers write it back
+    static constexpr bool LAST_DIRECT = (size_t)CW * PP * CHUNK_BYTES <= (size_t)NST * STAGE_BYTES;
     static_assert(2 * 2 * BLOCK_COLS <= 512, "two buffers x two consumer warps per lane quarter");
     static_assert(SMEM <= 227 * 1024, "v3 stages + park exceed shared memory");
     static_assert(NPARK % 2 == 0 && NPARK >= 4, "park slots hold chunk pairs");
@@ -179,6 +182,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         // ---------------- producer ----------------
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_PRODUCER) : "memory");
         if (threadIdx.x == 384) {
+            const uint64_t keep = l2_policy_evict_last();  // payload rows are re-read by many tiles
             int it = 0;
             for (int k = 0; k < my_tiles; ++k) {
                 const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
@@ -186,13 +190,36 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
                 const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
                 const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;
-                for (int w = 0; w < nb; ++w, ++it) {
+                if (P.hints & 4) {
+                    // pull the tile's slice lines into L2 ahead of its epilogue, so the
+                    // deferred reduces add into L2-resident lines instead of waiting on HBM
+#pragma unroll 1
+                    for (int cw = 0; cw < G::CW; ++cw) {
+                        const int wq = cw % G::CWQ, e0 = DD * (cw / G::CWQ);
+                        const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
+                        if (t.k1_0 + e0 + DD - 1 >= n || t.j0 + 31 + e0 + DD - 1 >= n || !P.use_gmap) continue;
+                        const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
+                        for (int pl = 0; pl < np; ++pl)
+                            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                                         ::"l"(reinterpret_cast<uint64_t>(&P.gmap)), "r"(2 * (t.j0 - t.k1_0 + n)),
+                                         "r"(t.k1_0 + e0), "r"(p_lo + pl) : "memory");
+                    }
+                }
+                for (int w = 0; w < nb && !(P.hints & 32); ++w, ++it) {
                     const int s = it % NST;
-                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    if (it >= NST) {
+                        if (P.hints & 64) mbar_wait_sleep(&empty[s], ((it / NST) - 1) & 1);
+                        else mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    }
                     mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
                     unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
-                    tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s]);
-                    tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
+                    if (P.hints & 2) {
+                        tma_load_3d_hint(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s], keep);
+                        tma_load_3d_hint(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s], keep);
+                    } else {
+                        tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s]);
+                        tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
+                    }
                 }
             }
         }
@@ -209,12 +236,16 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                                lane * (uint32_t)sizeof(Cx<R>);
         const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
         const uint64_t gmap = reinterpret_cast<uint64_t>(&P.gmap);
+        const uint64_t stream = l2_policy_evict_first();  // slice lines are touched once per pass
         int pair = 0;  // chunk pairs parked by this warp (slot = pair % NSLOT)
         constexpr int NSLOT = G::NPARK / 2;
-        for (int k = 0; k < my_tiles; ++k) {
+        const int drained = (!G::LAST_DIRECT || (P.hints & 1024)) ? my_tiles : my_tiles - 1;  // see consumers
+        for (int k = 0; k < drained && !(P.hints & 256); ++k) {
             const int b = k & 1;
-            mbar_wait(&tfull[b], (k >> 1) & 1);
+            if (P.hints & 64) mbar_wait_sleep(&tfull[b], (k >> 1) & 1);
+            else mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
+            if (P.trace && k < 32 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
             const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
@@ -242,10 +273,15 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                                      "r"(v[4 * i]), "r"(v[4 * i + 1]), "r"(v[4 * i + 2]), "r"(v[4 * i + 3]) : "memory");
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
                     __syncwarp();
-                    if (lane == 0) {
+                    if (lane == 0 && !(P.hints & 16)) {  // 16: lab only (no slice traffic)
                         const uint32_t sp = slot - lane * (uint32_t)sizeof(Cx<R>);
                         for (int c = 0; c < 2 && p + c < np; ++c) {
-                            if (box)  // one sheared box of the slice map: 32 entries x DD diagonals x 1 plane
+                            if (box && (P.hints & 1))  // one sheared box of the slice map: 32 x DD x 1
+                                asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+                                             ".L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(gmap),
+                                             "r"(sp + c * G::CHUNK_BYTES), "r"(c0), "r"(k1b), "r"(p_lo + p + c),
+                                             "l"(stream) : "memory");
+                            else if (box)
                                 asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
                                              " [%0, {%2, %3, %4}], [%1];" ::"l"(gmap), "r"(sp + c * G::CHUNK_BYTES),
                                              "r"(c0), "r"(k1b), "r"(p_lo + p + c) : "memory");
@@ -261,6 +297,27 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             tc_fence_before();
             __syncwarp();
+            if (P.trace && k < 32 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 1 + 6 * (q == 3)] = clock64();
+            if ((P.hints & 512) && k + 1 < drained) {
+                // lab: pull the next tile's slice lines of this warp's two blocks into L2
+                // (LSU prefetch, no TMA queue) so its reduces add into resident lines
+                const V3Tile tn = v3_tile<G>(P, (int)blockIdx.x + (k + 1) * (int)gridDim.x);
+                for (int h = 0; h < 2; ++h) {
+                    const int cw = q + 4 * h, wq = cw % G::CWQ, e0 = DD * (cw / G::CWQ);
+                    const int p_lo = (int)(tn.q0 - P.lo) + PP * wq;
+                    const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
+                    // segment (p, d) = 32 entries from (row k1b + d, column j0 + e0 + d): 5 lines of 128 B
+                    for (int i = lane; i < np * DD * 5; i += 32) {
+                        const int seg = i / 5, ln = i % 5, pl = seg / DD, d = seg % DD;
+                        const int k1 = tn.k1_0 + e0 + d;
+                        int k2 = tn.j0 + e0 + d;
+                        if (k1 >= n) continue;
+                        if (k2 >= n) k2 -= n;
+                        const Cx<R>* a = P.g4 + (int64_t)(p_lo + pl) * n * n + (int64_t)k1 * n + k2 + ln * 8;
+                        if (k2 + ln * 8 < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+                    }
+                }
+            }
             if (lane == 0) mbar_arrive(&tready[b]);
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -280,6 +337,8 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     const int e0 = DD * wr;
     const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (warp >> 2) * G::BLOCK_COLS;
     int it = 0;
+    int pend = -1;  // TMEM buffer whose stores are issued but not yet announced (tfull)
+    const bool defer_st = !(P.hints & 2048);
     for (int k = 0; k < my_tiles; ++k) {
         const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
         int ps = 0, pd = 0;
@@ -291,6 +350,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         }
         const int sh_o = (PP * wq + DR - DD - e0) * G::W + (31 - lane) + ps;  // band row of (p, d): + j * W
         const int dr_o = e0 * G::W + lane + pd;                                // direct row d: + d * W
+        if (P.trace && k < 32 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 4] = clock64();
         Cx<R> acc[PP][DD];
 #pragma unroll
         for (int p = 0; p < PP; ++p)
@@ -299,7 +359,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
 #pragma unroll 1
         for (int w = 0; w < nb; ++w, ++it) {
             const int s = it % NST;
-            mbar_wait(&full[s], (it / NST) & 1);
+            if (!(P.hints & 32)) mbar_wait(&full[s], (it / NST) & 1);  // 32: lab only (no fills at all)
             const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
             const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
             const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
@@ -323,13 +383,68 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             // release the stage once its values are consumed (see v2: the refill is
             // an async-proxy write, the last ld.shared may still be in flight)
+            if (!(P.hints & 128)) {  // 128: lab only (no stage release; needs 32)
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&empty[s]);
+            }
+            if (pend >= 0) {  // the previous tile's TMEM stores, overlapped with this first walker
+                tmem_wait_st();
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tfull[pend]);
+                pend = -1;
+            }
+        }
+        if (P.hints & 256) {  // lab only: no hand-off (the epilogue skips the tile too)
+            if (lane == 0 && acc[0][0].re == 1.2345) P.g4[0] = acc[PP - 1][DD - 1];
+            continue;
+        }
+        if (G::LAST_DIRECT && k == my_tiles - 1 && !(P.hints & 1024)) {
+            // The last tile: every stage is idle now (all fills consumed), so the
+            // eight warps park their blocks there and reduce them into the slice
+            // themselves, in parallel -- the kernel does not end on one epilogue
+            // warp's serial drain of a whole tile.
+            asm volatile("barrier.sync 2, %0;" ::"n"(32 * G::CW) : "memory");  // all stage reads done
+            const uint32_t park = smem_u32(smem_raw) + (uint32_t)warp * PP * G::CHUNK_BYTES;
+#pragma unroll
+            for (int p = 0; p < PP; ++p)
+#pragma unroll
+                for (int d = 0; d < DD; ++d)
+                    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(park + p * G::CHUNK_BYTES + (d * 32 + lane) * 16),
+                                 "d"(acc[p][d].re), "d"(acc[p][d].im) : "memory");
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) mbar_arrive(&empty[s]);
+            if (lane == 0) {
+                const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
+                const int k1b = t.k1_0 + e0;
+                const bool box = P.use_gmap && k1b + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n;
+                const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
+                for (int p = 0; p < np; ++p) {
+                    if (box)
+                        asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
+                                     " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&P.gmap)),
+                                     "r"(park + p * G::CHUNK_BYTES), "r"(2 * (t.j0 - t.k1_0 + n)), "r"(k1b),
+                                     "r"(p_lo + p) : "memory");
+                    else
+                        pst_edge_chunk(P, p_lo + p, k1b, t.j0 + e0, t.j0, DD,
+                                       reinterpret_cast<const Cx<double>*>(smem_raw + (park + p * G::CHUNK_BYTES -
+                                                                                       smem_u32(smem_raw))));
+                }
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // park read before exit
+            }
+            __syncwarp();
+            break;
         }
         // hand the block to the epilogue through TMEM buffer b
         const int b = k & 1;
-        if (k >= 2) mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
+        const long long tw0 = P.trace ? clock64() : 0;
+        if (k >= 2) {
+            if (P.hints & 64) mbar_wait_sleep(&tready[b], ((k >> 1) - 1) & 1);
+            else mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
+        }
+        if (P.trace && k < 32 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 3] = clock64() - tw0;
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < PP * DD / 8; ++c) {  // 8 entries (32 columns) per store
@@ -344,10 +459,16 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             tmem_st32(tq + b * 256 + c * 32, v);
         }
-        tmem_wait_st();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tfull[b]);
+        if (P.trace && k < 32 && lane == 0 && (warp == 0 || warp == 7))
+            P.trace[((size_t)blockIdx.x * 32 + k) * 8 + (warp == 0 ? 2 : 5)] = clock64();
+        pend = b;  // announced after the next tile's first walker (or below)
+        if (!defer_st || k == my_tiles - 1) {
+            tmem_wait_st();
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tfull[b]);
+            pend = -1;
+        }
     }
 }
 
@@ -378,6 +499,8 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         tp.off = sheared_offset(n, G::ES);
         G4_TRY(slice_map(g4p, n, hi - lo, 1, G::DD, &tp.gmap));
         tp.use_gmap = g4_gmap_enabled() ? 1 : 0;
+        static const int hints = env_int("G4RING_V3_HINTS", 0);  // A/B knob (lab)
+        tp.hints = hints;
         tp.nbatch = std::min(TMA_MAXW, nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
@@ -389,8 +512,25 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         const int64_t tiles = (int64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
         if (tiles >= (1ll << 31)) return fail(G4_ERR_CONTRACT, "accumulate: tile count too large");
         const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+        static const char* trace_path = getenv("G4RING_V3_TRACE");  // lab: per-tile timeline dump
+        long long* trace = nullptr;
+        if (trace_path) {
+            G4_CUDA(cudaMalloc(&trace, (size_t)grid * 32 * 8 * sizeof(long long)));
+            G4_CUDA(cudaMemsetAsync(trace, 0, (size_t)grid * 32 * 8 * sizeof(long long), st));
+            tp.trace = trace;
+        }
         kern<<<grid, G::THREADS, G::SMEM, st>>>(tp);
         G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_pst launch"));
+        if (trace) {
+            std::vector<long long> h((size_t)grid * 32 * 8);
+            G4_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));
+            G4_CUDA(cudaStreamSynchronize(st));
+            G4_CUDA(cudaFree(trace));
+            if (FILE* f = fopen(trace_path, "ab")) {
+                fwrite(h.data(), sizeof(long long), h.size(), f);
+                fclose(f);
+            }
+        }
     }
     return G4_OK;
 }

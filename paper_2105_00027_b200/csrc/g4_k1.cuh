@@ -97,6 +97,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Same, with a suspend-time hint: the waiting warp sleeps until the phase
+// completes (or 10 ms pass) instead of re-polling, so idle waiters -- the
+// epilogue and producer warps of K1 v3 -- do not take issue slots from the
+// consumer warps on their SM sub-partition.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, 10000000;\n\t"
+        "@!P bra WAIT_%=;\n}" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
 // 3-D tensor box -> shared memory, completion counted on an mbarrier.
 __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
                                             uint64_t* bar) {
@@ -105,6 +118,25 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, i
         " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
         : "memory");
+}
+// Same, with an L2 cache policy (createpolicy) on the loaded lines.
+__device__ __forceinline__ void tma_load_3d_hint(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                                 uint64_t* bar, uint64_t policy) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+        " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)), "l"(policy)
+        : "memory");
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_evict_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
 }
 // Same, delivered to every CTA of the cluster in `mask` (same smem offsets and
 // mbarrier offset in each destination CTA).
@@ -147,6 +179,9 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
     int32_t nx;   // plane chunks
     int32_t off;  // sheared-coordinate offset (elements), see make_maps
+    int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS): 1/2 L2 evict_first/last hints, 4 slice L2 prefetch,
+                    // 16 no slice write-back, 32 no payload fills (consumers compute on stale stages; timing only)
+    long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
 };
 
 // Shared -> global bulk copy by the TMA engine: add (.add reduction) or store.
