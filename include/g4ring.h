@@ -173,6 +173,9 @@ g4_status g4_ipc_close(void* dev_ptr);
 
 /* Stream-ordered peer copy (copy engine over NVLink/NVSwitch, or local). */
 g4_status g4_copy_async(void* dst, const void* src, int64_t bytes, void* stream);
+/* Copies that fell back from the strided peer form to whole staged payloads
+ * (a wire-format change, counted so a run can report it). */
+int64_t g4_peer_copy_fallbacks(void);
 /* The N x N cores (both spins) of `count` consecutive staged payloads, as one
  * strided peer copy: the ring's wire format.  The halo is not sent. */
 g4_status g4_copy_payload_cores(void* dst, const void* src, int32_t count, int32_t n, int32_t dtype,

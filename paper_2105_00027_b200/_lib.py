@@ -50,6 +50,7 @@ SIGNATURES = {
     "g4_ipc_import": (_i32, [_vp, _i64, _vpp]),
     "g4_ipc_close": (_i32, [_vp]),
     "g4_copy_async": (_i32, [_vp, _vp, _i64, _vp]),
+    "g4_peer_copy_fallbacks": (_i64, []),
     "g4_copy_payload_cores": (_i32, [_vp, _vp, _i32, _i32, _i32, _vp]),
     "g4_fill_halo": (_i32, [_vpp, _i32, _i32, _i32, _vp]),
     "g4_preload_ring_kernels": (_i32, []),

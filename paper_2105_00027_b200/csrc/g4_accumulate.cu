@@ -659,11 +659,17 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
         if (prm.n % 32 != 0 || nx % G::CL != 0)
             return launch_v2_t<R, RG, typename G::Base, FUSED, MINB, EXP>(prm, st);
     }
-    static bool attr_set = false;
-    if (!attr_set) {
-        G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-        attr_set = true;
+    {  // the >48 KB dynamic shared-memory opt-in is per device (a host may drive several GPUs)
+        static std::mutex mu;
+        static uint64_t done = 0;
+        int dev = 0;
+        G4_CUDA(cudaGetDevice(&dev));
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(done & (1ull << (dev & 63)))) {
+            G4_CUDA(cudaFuncSetAttribute(k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+            done |= 1ull << (dev & 63);
+        }
     }
     const int n = prm.n;
     for (int b0 = 0; b0 < prm.nbatch; b0 += TMA_MAXW) {

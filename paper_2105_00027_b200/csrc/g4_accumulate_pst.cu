@@ -190,21 +190,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
                 const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
                 const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;
-                if (P.hints & 4) {
-                    // pull the tile's slice lines into L2 ahead of its epilogue, so the
-                    // deferred reduces add into L2-resident lines instead of waiting on HBM
-#pragma unroll 1
-                    for (int cw = 0; cw < G::CW; ++cw) {
-                        const int wq = cw % G::CWQ, e0 = DD * (cw / G::CWQ);
-                        const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
-                        if (t.k1_0 + e0 + DD - 1 >= n || t.j0 + 31 + e0 + DD - 1 >= n || !P.use_gmap) continue;
-                        const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
-                        for (int pl = 0; pl < np; ++pl)
-                            asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
-                                         ::"l"(reinterpret_cast<uint64_t>(&P.gmap)), "r"(2 * (t.j0 - t.k1_0 + n)),
-                                         "r"(t.k1_0 + e0), "r"(p_lo + pl) : "memory");
-                    }
-                }
                 for (int w = 0; w < nb && !(P.hints & 32); ++w, ++it) {
                     const int s = it % NST;
                     if (it >= NST) {
@@ -298,26 +283,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             tc_fence_before();
             __syncwarp();
             if (P.trace && k < 32 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 1 + 6 * (q == 3)] = clock64();
-            if ((P.hints & 512) && k + 1 < drained) {
-                // lab: pull the next tile's slice lines of this warp's two blocks into L2
-                // (LSU prefetch, no TMA queue) so its reduces add into resident lines
-                const V3Tile tn = v3_tile<G>(P, (int)blockIdx.x + (k + 1) * (int)gridDim.x);
-                for (int h = 0; h < 2; ++h) {
-                    const int cw = q + 4 * h, wq = cw % G::CWQ, e0 = DD * (cw / G::CWQ);
-                    const int p_lo = (int)(tn.q0 - P.lo) + PP * wq;
-                    const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
-                    // segment (p, d) = 32 entries from (row k1b + d, column j0 + e0 + d): 5 lines of 128 B
-                    for (int i = lane; i < np * DD * 5; i += 32) {
-                        const int seg = i / 5, ln = i % 5, pl = seg / DD, d = seg % DD;
-                        const int k1 = tn.k1_0 + e0 + d;
-                        int k2 = tn.j0 + e0 + d;
-                        if (k1 >= n) continue;
-                        if (k2 >= n) k2 -= n;
-                        const Cx<R>* a = P.g4 + (int64_t)(p_lo + pl) * n * n + (int64_t)k1 * n + k2 + ln * 8;
-                        if (k2 + ln * 8 < n) asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-                    }
-                }
-            }
             if (lane == 0) mbar_arrive(&tready[b]);
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");

@@ -179,8 +179,9 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
     int32_t nx;   // plane chunks
     int32_t off;  // sheared-coordinate offset (elements), see make_maps
-    int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS): 1/2 L2 evict_first/last hints, 4 slice L2 prefetch,
-                    // 16 no slice write-back, 32 no payload fills (consumers compute on stale stages; timing only)
+    int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS, measurement only): 1/2 L2 evict_first/last hints,
+                    // 16 no slice write-back, 32 no payload fills, 64 sleeping waits, 128 no stage release,
+                    // 256 no TMEM hand-off, 1024 last tile via TMEM, 2048 TMEM-store wait not deferred
     long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
 };
 

@@ -6,6 +6,7 @@
 // (ringacc/transport/base.py:53-80: isend/irecv/PendingOp.wait) and its
 // reduce_sum collective (base.py:126-149) for device-resident buffers.
 #include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstring>
 #include <map>
@@ -65,6 +66,10 @@ __global__ void __launch_bounds__(256) k_reduce(const __grid_constant__ RedParam
 }
 
 }  // namespace g4
+
+namespace g4 {
+std::atomic<int64_t> g_peer_copy_fallbacks{0};  // see g4_copy_payload_cores
+}
 
 extern "C" {
 
@@ -147,6 +152,8 @@ g4_status g4_copy_async(void* dst, const void* src, int64_t bytes, void* stream)
     return G4_OK;
 }
 
+int64_t g4_peer_copy_fallbacks(void) { return g4::g_peer_copy_fallbacks.load(std::memory_order_relaxed); }
+
 // The N x N cores of `count` consecutive staged payloads (both spins), as one
 // strided copy-engine transfer: the halo (23 % of a payload at N = 512) never
 // crosses NVLink; the receiver rebuilds it (g4_fill_halo).
@@ -174,8 +181,10 @@ g4_status g4_copy_payload_cores(void* dst, const void* src, int32_t count, int32
         p.extent = ext;
         if (cudaMemcpy3DPeerAsync(&p, static_cast<cudaStream_t>(stream)) != cudaSuccess) {
             // no strided peer copy here: move whole staged payloads (the halo
-            // rebuild on the receiver is then a no-op rewrite)
+            // rebuild on the receiver is then a no-op rewrite).  Counted, so a run
+            // that silently changed its wire format shows it (g4_peer_copy_fallbacks).
             cudaGetLastError();
+            g_peer_copy_fallbacks.fetch_add(1, std::memory_order_relaxed);
             const int64_t bytes = (int64_t)2 * count * (int64_t)rows * (int64_t)pitch;
             G4_CUDA(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
                                     static_cast<cudaStream_t>(stream)));
@@ -213,12 +222,18 @@ g4_status g4_flag_wait(const void* flag, uint64_t value, void* stream) {
     // Where the device supports it, the wait also flushes outstanding remote
     // (NVLink peer) writes, so the payload that the flag announces is visible
     // to the K1 launch that follows on this stream.
-    static int flush = -1;
-    if (flush < 0) {
-        int dev = 0, v = 0;
-        flush = (cudaGetDevice(&dev) == cudaSuccess &&
-                 cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev) == cudaSuccess && v) ? 1 : 0;
+    // (a device attribute: cached per device, the ring may drive several GPUs
+    // from one process)
+    static std::atomic<int> flush_by_dev[64];  // 0 unknown, 1 no, 2 yes
+    int dev = 0;
+    G4_CUDA(cudaGetDevice(&dev));
+    int state = flush_by_dev[dev & 63].load(std::memory_order_relaxed);
+    if (state == 0) {
+        int v = 0;
+        state = (cudaDeviceGetAttribute(&v, cudaDevAttrCanFlushRemoteWrites, dev) == cudaSuccess && v) ? 2 : 1;
+        flush_by_dev[dev & 63].store(state, std::memory_order_relaxed);
     }
+    const bool flush = state == 2;
     const unsigned int how = CU_STREAM_WAIT_VALUE_GEQ | (flush ? CU_STREAM_WAIT_VALUE_FLUSH : 0u);
     CUresult r = fn(static_cast<CUstream>(stream), (CUdeviceptr)flag, (cuuint64_t)value, how);
     if (r != CUDA_SUCCESS) {

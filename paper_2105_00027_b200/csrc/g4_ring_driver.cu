@@ -66,10 +66,12 @@ struct Published {
     uint64_t flags_ptr, bufs_ptr[2], slice_ptr;
     int64_t pid;
     int32_t nch, lanes_mask;
+    int32_t device, reserved;  // CUDA ordinal of the allocations (same-process peers on other GPUs)
 };
 
 struct Ring {
     g4_ring_config cfg;
+    int device = 0;            // every entry point runs on the ring's own GPU
     int world_rank, S, pos, subring, n;
     int64_t lo, hi, next_round;
     int pcode;                 // staged payload dtype
@@ -111,10 +113,31 @@ static g4_status barrier(Ring* R, int32_t group, int members) {
     return gather(R, group, &one, 1, all.data());
 }
 
-// Peer pointer of a published allocation: direct within this process, else CUDA IPC.
+// Direct access from this rank's GPU to allocations on `peer` (same process,
+// another GPU): the copy engines' peer copies need it, and so do the flag
+// writes and the reduce kernel's loads through the raw pointers.
+static g4_status enable_peer(int self, int peer) {
+    if (peer == self) return G4_OK;
+    int can = 0;
+    G4_CUDA(cudaDeviceCanAccessPeer(&can, self, peer));
+    if (!can) {
+        set_error("GPU %d cannot access GPU %d directly (no peer path)", self, peer);
+        return G4_ERR_TRANSPORT;
+    }
+    const cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+    if (e == cudaErrorPeerAccessAlreadyEnabled) {
+        cudaGetLastError();
+        return G4_OK;
+    }
+    return check_cuda(e, "cudaDeviceEnablePeerAccess");
+}
+
+// Peer pointer of a published allocation: direct within this process (with peer
+// access enabled when it lives on another GPU), else CUDA IPC.
 static g4_status peer_ptr(Ring* R, const Published& p, const char* handle, int64_t off, uint64_t ptr,
                           uint64_t* out) {
     if (p.pid == (int64_t)getpid()) {
+        G4_TRY(enable_peer(R->device, p.device));
         *out = ptr;
         return G4_OK;
     }
@@ -169,6 +192,10 @@ g4_status g4_ring_create(const g4_ring_config* cfg, int32_t world_rank, g4_allga
 
     G4_TRY(g4_preload_ring_kernels());
     auto* R = new Ring();
+    if (cudaGetDevice(&R->device) != cudaSuccess) {
+        delete R;
+        return fail(G4_ERR_CUDA, "ring_create: no current CUDA device");
+    }
     R->cfg = *cfg;
     R->cfg.planes = planes;
     R->world_rank = world_rank;
@@ -243,6 +270,7 @@ g4_status g4_ring_create(const g4_ring_config* cfg, int32_t world_rank, g4_allga
     // publish flags / buffers / slice to the sub-ring, connect to the neighbours
     Published me{};
     me.pid = (int64_t)getpid();
+    me.device = R->device;
     me.nch = (int32_t)R->chans.size();
     RING_TRY(publish(R->flags, me.flags_h, &me.flags_off, &me.flags_ptr));
     for (size_t i = 0; i < R->chans.size(); ++i)
@@ -283,6 +311,7 @@ g4_status g4_ring_measure(void* ring, int64_t m, int32_t regenerate) {
     using namespace g4;
     auto* R = static_cast<Ring*>(ring);
     if (!R) return fail(G4_ERR_CONTRACT, "ring_measure: null ring");
+    G4_CUDA(cudaSetDevice(R->device));
     if (m != R->next_round) {
         set_error("rounds must be consecutive: expected %lld, got %lld", (long long)R->next_round, (long long)m);
         return G4_ERR_CONTRACT;
@@ -370,6 +399,7 @@ g4_status g4_ring_stage(void* ring, const void* const* up, const void* const* do
     using namespace g4;
     auto* R = static_cast<Ring*>(ring);
     if (!R || !up || !down) return fail(G4_ERR_CONTRACT, "ring_stage: null argument");
+    G4_CUDA(cudaSetDevice(R->device));
     std::vector<void*> ptrs;
     for (const Chan& c : R->chans)
         for (int i = 0; i < R->cfg.batch * (int)c.lanes.size(); ++i)
@@ -378,6 +408,12 @@ g4_status g4_ring_stage(void* ring, const void* const* up, const void* const* do
         set_error("ring_stage: expected %d payloads, got %d", (int)ptrs.size(), count);
         return G4_ERR_CONTRACT;
     }
+    // GEN still holds the previous round's payloads until their first ring copy
+    // has left (ev_sent, recorded on the comm stream): a slow neighbour keeps the
+    // comm stream waiting on ACK flags while the compute stream would run ahead
+    // (the same edge as g4_ring_measure's, and engine.RingEngine.stage_gen's).
+    if (R->next_round > 0 && R->S > 1)
+        for (const Chan& c : R->chans) G4_CUDA(cudaStreamWaitEvent(R->compute, R->ev_sent[c.index], 0));
     return g4_prepare_g(ptrs.data(), up, down, count, R->n, dtype_in, R->pcode, R->compute);
 }
 
@@ -385,6 +421,7 @@ g4_status g4_ring_wait(void* ring, int64_t timeout_ms) {
     using namespace g4;
     auto* R = static_cast<Ring*>(ring);
     if (!R) return fail(G4_ERR_CONTRACT, "ring_wait: null ring");
+    G4_CUDA(cudaSetDevice(R->device));
     std::vector<cudaStream_t> all = R->comm;
     all.push_back(R->compute);
     const auto t0 = std::chrono::steady_clock::now();
@@ -400,7 +437,11 @@ g4_status g4_ring_wait(void* ring, int64_t timeout_ms) {
                 // process can tear down (engine.RingEngine._raise_deadlock)
                 std::vector<int64_t> v(R->chans.size() * FLAGS_PER_CH);
                 cudaMemcpy(v.data(), R->flags, v.size() * 8, cudaMemcpyDeviceToHost);
-                const Chan& c = R->chans[0];
+                // the channel whose DATA flag lags the most is the stalled one
+                const Chan* lag = &R->chans[0];
+                for (const Chan& c : R->chans)
+                    if (v[c.index * FLAGS_PER_CH + F_DATA] < v[lag->index * FLAGS_PER_CH + F_DATA]) lag = &c;
+                const Chan& c = *lag;
                 const int64_t landed = v[c.index * FLAGS_PER_CH + F_DATA];
                 const int64_t k = std::max<int64_t>(landed + 1, FIRST_TRANSFER);
                 const int64_t per = std::max(R->S - 1, 1);
@@ -435,6 +476,7 @@ g4_status g4_ring_reduce(void* ring) {
     using namespace g4;
     auto* R = static_cast<Ring*>(ring);
     if (!R) return fail(G4_ERR_CONTRACT, "ring_reduce: null ring");
+    G4_CUDA(cudaSetDevice(R->device));
     const int groups = R->cfg.world_size / R->S;
     if (groups == 1) return G4_OK;
     G4_CUDA(cudaStreamSynchronize(R->compute));
@@ -449,6 +491,7 @@ g4_status g4_ring_reduce(void* ring) {
         for (int g = 1; g < groups && st == G4_OK; ++g) {
             const Published& q = pg[g];
             if (q.pid == (int64_t)getpid()) {
+                st = enable_peer(R->device, q.device);
                 src.push_back(reinterpret_cast<const void*>(q.slice_ptr));
             } else {
                 void* p = nullptr;
@@ -474,6 +517,7 @@ g4_status g4_ring_destroy(void* ring) {
     using namespace g4;
     auto* R = static_cast<Ring*>(ring);
     if (!R) return G4_OK;
+    cudaSetDevice(R->device);
     cudaStreamSynchronize(R->compute);
     for (cudaStream_t s : R->comm) cudaStreamSynchronize(s);
     // nobody may still be copying into (or reading) our buffers

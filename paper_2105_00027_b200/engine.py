@@ -617,19 +617,21 @@ class RingEngine:
             vals.copy_(self.flags, non_blocking=True)
         side.synchronize()
         s = self.cfg.subring_size
-        for c in self.channels:
-            landed = int(vals[c.index * S.FLAGS_PER_CHANNEL + S.DATA])
-            k = max(landed + 1, S.FIRST_TRANSFER)
-            m, j = divmod(k - S.FIRST_TRANSFER, max(s - 1, 1))
-            # unblock the streams so the process can tear down, then report
-            with torch.cuda.stream(side):
-                self.flags.fill_(1 << 62)
-            side.synchronize()
-            raise DeadlockError(f"rank {self.world_rank} lane {c.lanes[0]} stalled at measurement "
-                                f"{m * self.cfg.batch} step {j}: no payload from rank "
-                                f"{self.subring * s + c.recv_from}", rank=self.world_rank,
-                                lane=c.lanes[0], step=j)
-        raise DeadlockError(f"rank {self.world_rank} stalled", rank=self.world_rank)
+        # unblock the streams so the process can tear down, then report the channel
+        # whose DATA flag lags the most (with two directions either may be the stalled one)
+        with torch.cuda.stream(side):
+            self.flags.fill_(1 << 62)
+        side.synchronize()
+        if not self.channels:
+            raise DeadlockError(f"rank {self.world_rank} stalled", rank=self.world_rank)
+        landed = {c.index: int(vals[c.index * S.FLAGS_PER_CHANNEL + S.DATA]) for c in self.channels}
+        c = min(self.channels, key=lambda ch: landed[ch.index])
+        k = max(landed[c.index] + 1, S.FIRST_TRANSFER)
+        m, j = divmod(k - S.FIRST_TRANSFER, max(s - 1, 1))
+        raise DeadlockError(f"rank {self.world_rank} lane {c.lanes[0]} stalled at measurement "
+                            f"{m * self.cfg.batch} step {j}: no payload from rank "
+                            f"{self.subring * s + c.recv_from}", rank=self.world_rank,
+                            lane=c.lanes[0], step=j)
 
 
 # ---------------------------------------------------------------------------

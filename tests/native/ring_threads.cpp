@@ -1,19 +1,25 @@
 // tests/native/ring_threads.cpp -- a C++ host of the native ring driver (no
-// Python anywhere): every rank is a thread of this process, all on one GPU, and
-// the control plane is an in-process all-gather.  The reduced G4 (sub-ring 0's
+// Python anywhere): every rank is a thread of this process -- on one GPU, or
+// spread over every visible GPU (same-process peers on other devices: the
+// driver enables peer access) -- and the control plane is an in-process
+// all-gather.  The "fed" mode stages reference-layout walkers from the host
+// every round (g4_ring_stage) with rank 0 deliberately delayed, the case where
+// a stage could overwrite GEN before the previous round's payload left.  The reduced G4 (sub-ring 0's
 // slices) is checked bitwise against the C oracle (integer mode), i.e. against
 // the reference's serial sum over every walker of every lane and sub-ring.
 // TEST CODE: links the oracle (oracle/g4_oracle.c) as the checker.
 //
 // build: nvcc -std=c++17 -I include tests/native/ring_threads.cpp oracle/g4_oracle.c \
 //          -L paper_2105_00027_b200 -lg4ring -Xlinker -rpath=paper_2105_00027_b200 -o ring_threads
-// run:   ./ring_threads [world] [subring] [lanes] [alternate] [batch] [rounds]
+// run:   ./ring_threads [world] [subring] [lanes] [alternate] [batch] [rounds] [devices] [fed] [delay_ms]
+//        devices: 1 = all ranks on GPU 0, 0 = round-robin over every visible GPU
 #include <condition_variable>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <chrono>
 #include <thread>
 #include <vector>
 
@@ -82,6 +88,15 @@ int main(int argc, char** argv) {
     const int alternate = argc > 4 ? std::atoi(argv[4]) : 1;
     const int batch = argc > 5 ? std::atoi(argv[5]) : 2;
     const int rounds = argc > 6 ? std::atoi(argv[6]) : 3;
+    const int one_gpu = argc > 7 ? std::atoi(argv[7]) : 1;
+    const int fed = argc > 8 ? std::atoi(argv[8]) : 0;
+    const int delay_ms = argc > 9 ? std::atoi(argv[9]) : 0;
+    int ngpu = 1;
+    if (!one_gpu && cudaGetDeviceCount(&ngpu) != cudaSuccess) ngpu = 1;
+    if (fed && alternate) {
+        std::fprintf(stderr, "fed mode stages one channel (alternate = 0)\n");
+        return 1;
+    }
     g4_ring_config cfg{};
     cfg.n_k = 4;
     cfg.n_w = 8;
@@ -106,11 +121,44 @@ int main(int argc, char** argv) {
     std::vector<std::thread> threads;
     for (int r = 0; r < world; ++r) {
         threads.emplace_back([&, r] {
-            cudaSetDevice(0);
+            cudaSetDevice(r % ngpu);
             RankCtx ctx{{sub[r / S], pos[r % S]}, {r % S, r / S}};
             void* ring = nullptr;
             CHECK(g4_ring_create(&cfg, r, allgather, &ctx, &ring));
-            for (int m = 0; m < rounds; ++m) CHECK(g4_ring_measure(ring, m, 1));
+            if (!fed) {
+                for (int m = 0; m < rounds; ++m) CHECK(g4_ring_measure(ring, m, 1));
+            } else {
+                // host-fed: reference-layout walkers staged every round (one channel:
+                // batch-major, lanes in order), rank 0 late on every round; no wait
+                // between rounds, so the other ranks stage round m + 1 while their
+                // comm streams still wait for rank 0 to take round m
+                const int cnt = batch * lanes;
+                std::vector<double> hu((size_t)n * n * 2), hd((size_t)n * n * 2);
+                std::vector<void*> du((size_t)cnt * rounds), dd((size_t)cnt * rounds);
+                for (size_t i = 0; i < du.size(); ++i) {
+                    cudaMalloc(&du[i], hu.size() * 8);
+                    cudaMalloc(&dd[i], hd.size() * 8);
+                }
+                for (int m = 0; m < rounds; ++m) {
+                    if (r == 0 && delay_ms) std::this_thread::sleep_for(std::chrono::milliseconds(delay_ms));
+                    for (int b = 0; b < batch; ++b)
+                        for (int t = 0; t < lanes; ++t) {
+                            g4o_fill_gsigma(cfg.seed, r, t, (int64_t)m * batch + b, n, G4_MODE_INTEGER, hu.data(),
+                                            hd.data());
+                            const size_t i = (size_t)m * cnt + b * lanes + t;  // per-round buffers
+                            cudaMemcpy(du[i], hu.data(), hu.size() * 8, cudaMemcpyHostToDevice);
+                            cudaMemcpy(dd[i], hd.data(), hd.size() * 8, cudaMemcpyHostToDevice);
+                        }
+                    CHECK(g4_ring_stage(ring, du.data() + (size_t)m * cnt, dd.data() + (size_t)m * cnt, cnt,
+                                        G4_C128));
+                    CHECK(g4_ring_measure(ring, m, 0));
+                }
+                CHECK(g4_ring_wait(ring, 60000));
+                for (size_t i = 0; i < du.size(); ++i) {
+                    cudaFree(du[i]);
+                    cudaFree(dd[i]);
+                }
+            }
             CHECK(g4_ring_wait(ring, 60000));
             CHECK(g4_ring_reduce(ring));
             if (r < S) {
@@ -143,7 +191,8 @@ int main(int argc, char** argv) {
             return 2;
         }
     }
-    std::printf("ring_threads ok: world %d, sub-rings of %d, %d lanes%s, %d rounds x %d walkers, N=%d\n", world,
-                S, lanes, alternate ? " (alternate)" : "", rounds, batch, n);
+    std::printf("ring_threads ok: world %d, sub-rings of %d, %d lanes%s, %d rounds x %d walkers, N=%d, "
+                "%d GPU(s)%s\n", world, S, lanes, alternate ? " (alternate)" : "", rounds, batch, n, ngpu,
+                fed ? ", host-fed" : "");
     return 0;
 }

@@ -2,7 +2,9 @@
 are threads of one process sharing the GPU, the control plane an in-process
 all-gather, no Python on the path.  Compiled with nvcc and linked against
 libg4ring.so; its reduced G4 is checked bitwise against the C oracle inside the
-program.  GPU only."""
+program.  Also: ranks spread over every visible GPU (one GPU on the test box:
+the same code path with peer access to itself), and host-fed rounds
+(g4_ring_stage every round) with rank 0 delayed.  GPU only."""
 import subprocess
 
 import pytest
@@ -28,7 +30,10 @@ def ring_threads(tmp_path_factory):
 
 @pytest.mark.parametrize("args", [["4", "2", "2", "1", "2", "3"],    # 2 sub-rings of 2, alternate lanes
                                   ["3", "3", "1", "0", "1", "2"],    # one ring of 3
-                                  ["2", "1", "2", "0", "2", "2"]])   # S = 1: replicas + reduce
+                                  ["2", "1", "2", "0", "2", "2"],    # S = 1: replicas + reduce
+                                  ["4", "4", "2", "1", "1", "3", "0"],             # ranks over every visible GPU
+                                  ["4", "4", "2", "0", "2", "4", "1", "1", "30"],  # host-fed, rank 0 late
+                                  ["3", "3", "1", "0", "1", "3", "0", "1", "15"]])
 def test_cpp_host_ring(ring_threads, args):
     out = subprocess.run([str(ring_threads), *args], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stderr
