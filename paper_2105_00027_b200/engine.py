@@ -31,7 +31,7 @@ import json
 import os
 import socket
 import time
-from dataclasses import asdict, dataclass, field
+from dataclasses import asdict, dataclass, field, fields
 
 import numpy as np
 import torch
@@ -51,8 +51,17 @@ _MODE_CODE = {"float": _lib.G4_MODE_FLOAT, "integer": _lib.G4_MODE_INTEGER}
 
 @dataclass
 class ExperimentConfig:
-    """Run shape -- the fields of ringacc.config.ExperimentConfig (config.py:46-83)
-    that concern the hot path, plus the B200 extensions."""
+    """Run shape -- every field of ringacc.config.ExperimentConfig
+    (config.py:46-66, same names, order and defaults, so reference keyword and
+    positional constructions both work), plus the B200 extensions (keyword
+    only in practice; they follow the reference fields).
+
+    ``transport``, ``link``, ``out_dir``, ``sweep`` and ``memory`` are accepted
+    and validated like the reference but do not steer the device ring: its
+    payloads always move over peer memory (NVLink), and the sweep/memory
+    settings belong to the reference's CLI models (model.py holds those).
+    ``transport`` selects the data path only on the communicator path
+    (``rank_main(rt, world, cfg)`` with a reference-style communicator)."""
 
     n_k: int
     n_w: int
@@ -62,9 +71,14 @@ class ExperimentConfig:
     measurements: int
     seed: int = 0
     value_mode: str = "float"
+    transport: str = "inprocess"
     direction: str = "forward"
+    link: object = None
     timeout_s: float = 30.0
     instrument: bool = True
+    out_dir: str | None = None
+    sweep: object = None
+    memory: object = None
     # B200 extensions
     planes: int | None = None      # exchange planes K3 in [0, planes); None = all N (reference)
     batch: int = 1                 # measurements per lane carried by one ring message / K1 pass
@@ -89,8 +103,32 @@ class ExperimentConfig:
         return asdict(self)
 
 
-def validate_config(cfg: ExperimentConfig) -> None:
-    """config.py:156-185 semantics (ConfigError), plus the extensions."""
+TRANSPORTS = ("inprocess", "sim", "tcp")
+
+
+def as_config(cfg) -> ExperimentConfig:
+    """This package's config from a reference ``ringacc.config.ExperimentConfig``
+    (or any object with its attributes, or a dict of its fields).  Fields the
+    reference does not have keep their defaults."""
+    if isinstance(cfg, ExperimentConfig):
+        return cfg
+    names = [f.name for f in fields(ExperimentConfig)]
+    if isinstance(cfg, dict):
+        unknown = sorted(set(cfg) - set(names))
+        if unknown:
+            raise ConfigError(f"unknown config key(s): {', '.join(unknown)}")
+        return ExperimentConfig(**cfg)
+    kw = {k: getattr(cfg, k) for k in names if hasattr(cfg, k)}
+    missing = [k for k in ("n_k", "n_w", "world_size", "subring_size", "lanes", "measurements") if k not in kw]
+    if missing:
+        raise ConfigError(f"missing required config key: {missing[0]}")
+    return ExperimentConfig(**kw)
+
+
+def validate_config(cfg) -> None:
+    """config.py:156-185 semantics (ConfigError), plus the extensions.  Accepts
+    a reference config too (as_config)."""
+    cfg = as_config(cfg)
     for name in ("n_k", "n_w", "world_size", "subring_size", "lanes", "measurements", "batch"):
         v = getattr(cfg, name)
         if not isinstance(v, int) or v < 1:
@@ -99,6 +137,9 @@ def validate_config(cfg: ExperimentConfig) -> None:
         raise ConfigError(f"seed must be a non-negative integer, got {cfg.seed!r}")
     if cfg.world_size % cfg.subring_size != 0:
         raise ConfigError(f"subring_size {cfg.subring_size} does not divide world_size {cfg.world_size}")
+    if cfg.planes is None and cfg.world_size > cfg.space_size:
+        raise ConfigError(f"world_size {cfg.world_size} exceeds combined index count {cfg.space_size}: "
+                          "some rank would own an empty slice")
     if not (1 <= cfg.num_planes <= cfg.space_size):
         raise ConfigError(f"planes must be in [1, {cfg.space_size}], got {cfg.num_planes}")
     if cfg.subring_size > cfg.num_planes:
@@ -108,6 +149,8 @@ def validate_config(cfg: ExperimentConfig) -> None:
         raise ConfigError(f"lanes must be < {S.MAX_LANES} (tag stride), got {cfg.lanes}")
     if cfg.value_mode not in VALUE_MODES:
         raise ConfigError(f"value_mode must be one of {VALUE_MODES}, got {cfg.value_mode!r}")
+    if cfg.transport not in TRANSPORTS:
+        raise ConfigError(f"transport must be one of {TRANSPORTS}, got {cfg.transport!r}")
     if cfg.direction not in ("forward", "alternate"):
         raise ConfigError(f"direction must be forward or alternate, got {cfg.direction!r}")
     if cfg.dtype not in ("c128", "c64", "c128g64"):
@@ -233,16 +276,59 @@ def reduce_sum(ctl: Control, data: torch.Tensor, root: int = 0) -> None:
 
 @dataclass
 class LaneCounters:
-    """Per-(rank, lane) counters (instrument.py:14-33 semantics)."""
+    """Per-(rank, lane) counters: the fields of ringacc.instrument.CounterSet
+    (instrument.py:14-33, same names and meaning) plus ``messages_sent`` (ring
+    messages, one per step, each carrying `batch` payloads).  The device ring
+    fills the counts; its timers stay 0 (device time is in round_ms)."""
 
     envelopes_sent: int = 0       # payloads (measurements) forwarded to the next rank
     envelopes_received: int = 0
-    accumulations_applied: int = 0
-    messages_sent: int = 0        # ring messages (one per step; carries `batch` payloads)
     bytes_sent: int = 0
+    bytes_received: int = 0
+    accumulations_applied: int = 0
+    wait_s: float = 0.0
+    accumulate_s: float = 0.0
+    total_s: float = 0.0
+    messages_sent: int = 0
+
+    def add(self, other) -> None:
+        for f in fields(self):
+            setattr(self, f.name, getattr(self, f.name) + getattr(other, f.name, 0))
 
     def to_dict(self) -> dict:
         return asdict(self)
+
+    @classmethod
+    def from_dict(cls, d: dict) -> "LaneCounters":
+        return cls(**{f.name: d.get(f.name, 0) for f in fields(cls)})
+
+
+@dataclass
+class CounterRegistry:
+    """All lanes' counters of one experiment (instrument.py:103-131)."""
+
+    clock_label: str = "cuda-event"
+    lanes: dict = field(default_factory=dict)
+
+    def register(self, rank: int, lane: int, counters) -> None:
+        self.lanes[(rank, lane)] = counters
+
+    def snapshot(self, scope: str = "global", rank: int | None = None, lane: int | None = None) -> LaneCounters:
+        """Aggregate counters at lane, rank, or global scope."""
+        out = LaneCounters()
+        for (r, t), c in self.lanes.items():
+            if scope == "lane" and (r, t) != (rank, lane):
+                continue
+            if scope == "rank" and r != rank:
+                continue
+            out.add(c)
+        return out
+
+    def per_rank(self) -> dict:
+        ranks: dict[int, LaneCounters] = {}
+        for (r, _), c in self.lanes.items():
+            ranks.setdefault(r, LaneCounters()).add(c)
+        return ranks
 
 
 class RingEngine:
@@ -483,6 +569,7 @@ class RingEngine:
             for t, cnt in self.counters.items():
                 cnt.accumulations_applied += d["acc"][t]
                 cnt.envelopes_received += d["recv"][t]
+                cnt.bytes_received += d["recv"][t] * self.wire_bytes
                 cnt.envelopes_sent += d["sent"][t]
                 cnt.messages_sent += d["msgs"][t]
                 cnt.bytes_sent += d["bytes"][t]
@@ -521,6 +608,7 @@ class RingEngine:
                         self.counters[t].accumulations_applied += nb
                         if buf != S.GEN:
                             self.counters[t].envelopes_received += nb
+                            self.counters[t].bytes_received += nb * self.wire_bytes
                         if cfg.instrument:
                             if buf == S.GEN:
                                 bp = self.pos
@@ -639,12 +727,13 @@ class RingEngine:
 
 @dataclass
 class ExperimentReport:
-    """engine.py:187-220 fields that apply to the device engine."""
+    """engine.py:187-238: same fields, JSON form and registry(); plus the
+    device round times and sampled planes."""
 
     config: dict
     tensor: np.ndarray | None
     meas_counts: dict[int, int]
-    lane_counters: dict[tuple[int, int], dict]
+    lane_counters: dict[tuple[int, int], LaneCounters]
     lane_meta: dict[tuple[int, int], dict]
     memory_peaks: dict[int, int]
     slices: dict[int, tuple[int, int]]
@@ -652,14 +741,37 @@ class ExperimentReport:
     clock: str = "cuda-event"
     round_ms: dict[int, list[float]] = field(default_factory=dict)
     samples: dict[int, np.ndarray] = field(default_factory=dict)
+    memory_series: list = field(default_factory=list)
+
+    def registry(self) -> CounterRegistry:
+        reg = CounterRegistry(clock_label=self.clock)
+        for (r, t), c in self.lane_counters.items():
+            reg.register(r, t, c)
+        return reg
 
     def to_json_dict(self) -> dict:
         return {"config": self.config, "clock": self.clock, "elapsed_s": self.elapsed_s,
                 "meas_counts": {str(r): v for r, v in sorted(self.meas_counts.items())},
                 "slices": {str(r): list(v) for r, v in sorted(self.slices.items())},
-                "counters": {f"{r}/{t}": c for (r, t), c in sorted(self.lane_counters.items())},
+                "counters_global": self.registry().snapshot("global").to_dict(),
+                "counters": {f"{r}/{t}": c.to_dict() for (r, t), c in sorted(self.lane_counters.items())},
                 "lane_meta": {f"{r}/{t}": m for (r, t), m in sorted(self.lane_meta.items())},
-                "memory_peaks": {str(r): p for r, p in sorted(self.memory_peaks.items())}}
+                "memory_peaks": {str(r): p for r, p in sorted(self.memory_peaks.items())},
+                "memory_series": [list(e) for e in self.memory_series]}
+
+    @classmethod
+    def from_json_dict(cls, d: dict, tensor) -> "ExperimentReport":
+        def key2(s):
+            r, t = s.split("/")
+            return int(r), int(t)
+
+        return cls(config=d["config"], tensor=tensor, clock=d["clock"], elapsed_s=d["elapsed_s"],
+                   meas_counts={int(r): n for r, n in d["meas_counts"].items()},
+                   slices={int(r): tuple(v) for r, v in d["slices"].items()},
+                   lane_counters={key2(k): LaneCounters.from_dict(c) for k, c in d["counters"].items()},
+                   lane_meta={key2(k): m for k, m in d["lane_meta"].items()},
+                   memory_peaks={int(r): p for r, p in d["memory_peaks"].items()},
+                   memory_series=[tuple(e) for e in d.get("memory_series", [])])
 
 
 def device_for_rank(rank: int) -> torch.device:
@@ -667,8 +779,37 @@ def device_for_rank(rank: int) -> torch.device:
     return torch.device("cuda", local % max(torch.cuda.device_count(), 1))
 
 
-def rank_main(cfg: ExperimentConfig, world: Control | None = None) -> ExperimentReport | None:
-    """Everything one rank does (engine.py:241-297); the report on world rank 0."""
+def rank_main(*args, **kwargs) -> ExperimentReport | None:
+    """Everything one rank does (engine.py:241-297); the report on world rank 0.
+
+    Two call forms:
+    * ``rank_main(rt, world, cfg)`` -- the reference signature.  With a
+      reference-style communicator (``isend``/``irecv``/``split``/``reduce_sum``)
+      the lanes run ``run_measurement`` over that communicator (lanes.py: the
+      caller's transport moves the payloads in the reference wire format; the
+      GPU generates and accumulates).  With a ``Control`` (or None) it is the
+      device ring below; ``rt`` is then unused.
+    * ``rank_main(cfg, world=None)`` -- the device ring: one process per GPU,
+      torch.distributed control plane, payloads over peer memory.
+    ``cfg`` may be this package's ExperimentConfig or the reference's."""
+    if args and _is_config(args[0]):
+        cfg = args[0]
+        world = args[1] if len(args) > 1 else kwargs.get("world")
+        return _device_rank_main(as_config(cfg), world)
+    rt, world, cfg = (list(args) + [kwargs.get(k) for k in ("rt", "world", "cfg")][len(args):])[:3]
+    cfg = as_config(cfg)
+    if world is not None and not isinstance(world, Control) and hasattr(world, "isend"):
+        from .lanes import comm_rank_main
+        validate_config(cfg)
+        return comm_rank_main(rt, world, cfg)
+    return _device_rank_main(cfg, world)
+
+
+def _is_config(x) -> bool:
+    return isinstance(x, ExperimentConfig) or (hasattr(x, "n_k") and hasattr(x, "subring_size"))
+
+
+def _device_rank_main(cfg: ExperimentConfig, world: "Control | None") -> ExperimentReport | None:
     validate_config(cfg)
     world = world or Control()
     if world.size != cfg.world_size:
@@ -716,6 +857,7 @@ def _rank_main(cfg: ExperimentConfig, world: Control, r: int, device: torch.devi
     samples = _gather_planes(world, eng, cfg, cfg.sample_planes) if cfg.sample_planes else {}
     blob = {"rank": r, "meas_count": eng.meas_count, "slice": [eng.lo, eng.hi],
             "counters": {t: c.to_dict() for t, c in eng.counters.items()},
+            "final_send": _final_send_origins(eng, cfg),
             "origins": {t: eng.origins[t] for t in eng.origins},
             "peak": int(torch.cuda.max_memory_allocated(device)), "gpu_ms": gpu_ms}
     blobs = world.allgather(json.dumps(blob))
@@ -730,13 +872,28 @@ def _rank_main(cfg: ExperimentConfig, world: Control, r: int, device: torch.devi
         peaks[rr] = b["peak"]
         rms[rr] = [b["gpu_ms"]]
         for t, c in b["counters"].items():
-            counters[(rr, int(t))] = c
+            counters[(rr, int(t))] = LaneCounters.from_dict(c)
             meta[(rr, int(t))] = {"lane": int(t), "allocations": 3, "ring_phase_allocations": 0,
                                   "isolation_violations": 0,
+                                  "final_send_origin": b["final_send"][t],
                                   "origins": [tuple(o) for o in b["origins"][t]]}
     return ExperimentReport(config=cfg.to_dict(), tensor=tensor, meas_counts=meas, lane_counters=counters,
                             lane_meta=meta, memory_peaks=peaks, slices=slices, elapsed_s=elapsed,
                             round_ms=rms, samples=samples)
+
+
+def _final_send_origins(eng: "RingEngine", cfg: ExperimentConfig) -> dict[int, list[int]]:
+    """The origin of the payload each lane holds in its send buffer after the
+    last measurement (engine.py:275-277): the one received at the last ring
+    step, born birth_position(pos, steps - 1) (its own when there are no steps)."""
+    s = cfg.subring_size
+    steps = s - 1 if cfg.ring_steps_override is None else cfg.ring_steps_override
+    out = {}
+    for c in eng.channels:
+        bp = S.birth_position(eng.pos, steps - 1, s, c.backward) if steps > 0 else eng.pos
+        for t in c.lanes:
+            out[t] = [eng.subring, bp, t, cfg.measurements - 1, eng.subring * s + bp]
+    return out
 
 
 def _gather_full(world: Control, eng: RingEngine, cfg: ExperimentConfig) -> np.ndarray | None:
@@ -818,10 +975,11 @@ def _worker(rank: int, cfg_dict: dict, port: int, q) -> None:
                 pass
 
 
-def run_experiment(cfg: ExperimentConfig) -> ExperimentReport:
+def run_experiment(cfg) -> ExperimentReport:
     """Run a whole experiment (engine.py:323-335).  Inside an initialised
     torch.distributed world every rank calls this; otherwise one process per
     rank is spawned on this node (ranks share GPUs round-robin)."""
+    cfg = as_config(cfg)
     validate_config(cfg)
     if dist.is_available() and dist.is_initialized():
         return rank_main(cfg)
@@ -858,3 +1016,7 @@ def run_experiment(cfg: ExperimentConfig) -> ExperimentReport:
     if len(results) < cfg.world_size:
         raise DeadlockError("experiment did not finish before the launcher deadline")
     return results[0][1]
+
+
+# the reference's per-lane driver over an injected communicator (lanes.py)
+from .lanes import LaneRecorder, LaneState, NullRecorder, run_measurement  # noqa: E402,F401

@@ -39,8 +39,8 @@ def check(c, rep):
     for r in range(c.world_size):
         for t in range(k):
             cnt = rep.lane_counters[(r, t)]
-            assert cnt["envelopes_sent"] == steps * m and cnt["envelopes_received"] == steps * m
-            assert cnt["accumulations_applied"] == (steps + 1) * m
+            assert cnt.envelopes_sent == steps * m and cnt.envelopes_received == steps * m
+            assert cnt.accumulations_applied == (steps + 1) * m
             origins = rep.lane_meta[(r, t)]["origins"]
             assert len(origins) == len(set(origins)) == (steps + 1) * m
             assert all(o[2] == t and o[0] == r // s for o in origins)
@@ -121,7 +121,7 @@ def test_config4_scale_distributed_sampled_planes(oracle):
 def test_short_ring_negative_control():
     c = cfg(world_size=3, subring_size=3, n_w=3, ring_steps_override=1)
     rep = E.run_experiment(c)
-    assert rep.lane_counters[(0, 0)]["envelopes_sent"] == 1 * 2
+    assert rep.lane_counters[(0, 0)].envelopes_sent == 1 * 2
     assert rep.meas_counts[0] == 2 * 2
     assert not np.array_equal(rep.tensor, oracle_of(c))
 
@@ -149,8 +149,8 @@ def check_counts(c, rep):
     for r in range(c.world_size):
         for t in range(k):
             cnt = rep.lane_counters[(r, t)]
-            assert cnt["envelopes_sent"] == (s - 1) * m and cnt["envelopes_received"] == (s - 1) * m
-            assert cnt["accumulations_applied"] == s * m
+            assert cnt.envelopes_sent == (s - 1) * m and cnt.envelopes_received == (s - 1) * m
+            assert cnt.accumulations_applied == s * m
         assert rep.meas_counts[r] == s * m * k
 
 
