@@ -321,7 +321,7 @@ def run_gpu(args):
     achieved = alg_bytes / (statistics.mean(k_ms) * 1e-3) / 1e9
 
     # -- e2e: reference-layout payloads in pinned host memory through g4_accumulate --
-    e2e = run_e2e(args, lib, T, sp, planes, dtype, eb, dev)
+    e2e = None if args.skip_extras else run_e2e(args, lib, T, sp, planes, dtype, eb, dev)
     # -- the timed kernel's output, checked after timing (sampled planes vs the C oracle) --
     parity = parity_check(T, sl, pools[0], planes, n, dtype, args.arith)
 
@@ -343,12 +343,17 @@ def run_gpu(args):
         "e2e": e2e,
         "parity_check": parity,
         "gpu_launches": args.steps,
-        "batch_sweep": batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B),
-        "other_arith": other_arith_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B,
-                                         args.arith),
         "g4_bytes": sl.nbytes,
-        "max_g4": max_g4_capacity(dev, walkers=B),
     }
+    if not args.skip_extras:
+        line["batch_sweep"] = batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B)
+        line["other_arith"] = other_arith_point(lib, _lib, T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B,
+                                                args.arith)
+        line["max_g4"] = max_g4_capacity(dev, walkers=B)
+    if args.config == "c2" and not args.planes and not args.skip_extras:
+        del sl, pools
+        torch.cuda.empty_cache()
+        line["config_points"] = config_points(T, dev, dtype, pdtype, eb, peb, peak)
     if not args.no_cpu_baseline:
         from oracle import oracle as O
         cores = O.cpu_count()
@@ -439,6 +444,51 @@ def batch_sweep(T, sl, sp, pdtype, dev, planes, n, eb, peb, peak, B_main, batche
         byt = 2 * planes * n * n * eb + B * 2 * n * n * peb
         out[str(B)] = {"updates_per_s": B * planes * n * n / s, "hbm_frac": byt / s / 1e9 / peak,
                        "us_per_pass": s * 1e6}
+    return out
+
+
+# Per-GPU K1 work of the other BASELINE configs, timed on this GPU like the headline
+# (secondary points; the 8-GPU runs themselves need an 8-GPU node):
+# (name, n_k, n_w, planes, walkers per pass, description)
+CONFIG_POINTS = [
+    ("c3_share", 16, 64, 16, 16, "config 3 per-GPU K1 pass: N=1024, 64 planes over sub-rings of 4 -> 16 planes, "
+                                 "2 lanes x 8 walkers in one pass"),
+    ("c3_full", 16, 64, 64, 8, "config 3 index space on one GPU: N=1024, all 64 planes, 8 walkers"),
+    ("c4_share", 36, 128, 72, 8, "config 4 per-GPU share of the 8-GPU ring: N=4608, 72 planes (24.5 GB), "
+                                 "8 walkers"),
+]
+
+
+def config_points(T, dev, dtype, pdtype, eb, peb, peak, steps=5):
+    """K1 throughput and HBM fraction for each CONFIG_POINTS entry: its own
+    slice and two walker pools (alternating), >= 3 warm-up passes, event-timed
+    back-to-back passes."""
+    import torch
+    out = {}
+    for name, n_k, n_w, planes, B, desc in CONFIG_POINTS:
+        sp = T.CombinedIndexSpace(n_k, n_w)
+        n = sp.size
+        sl = T.GtSlice.zeros(sp, 0, planes, device=dev, dtype=dtype)
+        pools = [[T.GSigma.empty(sp, device=dev, dtype=pdtype) for _ in range(B)] for _ in range(2)]
+        for i, pool in enumerate(pools):
+            T.fill_gsigmas(pool, 2, [T.Origin(0, 0, w, 50 + i, 0) for w in range(B)], "float")
+        for i in range(3):
+            T.accumulate_g4_batch(sl, pools[i % 2])
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        a.record()
+        for i in range(steps):
+            T.accumulate_g4_batch(sl, pools[i % 2])
+        b.record()
+        torch.cuda.synchronize(dev)
+        t = a.elapsed_time(b) * 1e-3 / steps
+        byt = 2 * planes * n * n * eb + B * 2 * n * n * peb
+        out[name] = {"workload": desc, "n": n, "planes": planes, "walkers_per_pass": B,
+                     "updates_per_s": B * planes * n * n / t, "hbm_frac": byt / t / 1e9 / peak,
+                     "us_per_pass": t * 1e6, "g4_bytes": sl.nbytes,
+                     "l2": "slice larger than L2" if sl.nbytes > 126e6 else "slice fits L2 (L2-resident caveat)"}
+        del sl, pools
+        torch.cuda.empty_cache()
     return out
 
 
@@ -685,10 +735,12 @@ def run_ring(args):
     torch.cuda.synchronize(dev)
     eng.kernel_events = []
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    nvl = NvlinkCounters(dev.index)
     with ClockSampler(dev.index) as clk:
         time.sleep(0.3)
         world.barrier()
         torch.cuda.synchronize(dev)
+        nvl.start()
         t0.record(eng.compute)
         h0 = time.perf_counter()
         for i in range(args.steps):
@@ -697,10 +749,14 @@ def run_ring(args):
         t1.record(eng.compute)
         eng.wait_idle(300.0)
         torch.cuda.synchronize(dev)
+        nvl.stop()
         world.barrier()
     ms_local = t0.elapsed_time(t1) / args.steps
+    props = torch.cuda.get_device_properties(dev)
     stats = world.allgather({"ms": ms_local, "k_ms": eng.k1_mean_ms(), "clk": clk.summary(),
-                             "lo": eng.lo, "hi": eng.hi, "host_ms": host_ms})
+                             "lo": eng.lo, "hi": eng.hi, "host_ms": host_ms, "nvlink": nvl.result(args.steps),
+                             "device": {"index": dev.index, "pci_bus_id": getattr(props, "pci_bus_id", None),
+                                        "uuid": str(getattr(props, "uuid", ""))}})
     e2e = run_ring_e2e(args, eng, world, dev)
     eng_native = eng.native
     eng_wire_cores = eng.wire_cores
@@ -726,16 +782,24 @@ def run_ring(args):
         "data": "synthetic (reference counter-based generator on device, float mode, seed 0; resident)",
         "config": workload_config(args, n_ranks),
         "devices": {"visible": torch.cuda.device_count(), "ranks": n_ranks,
-                    "ranks_per_device": -(-n_ranks // max(torch.cuda.device_count(), 1))},
+                    "ranks_per_device": -(-n_ranks // max(torch.cuda.device_count(), 1)),
+                    "rank_devices": [x["device"] for x in stats],
+                    "comm": "torch.distributed gloo control plane (no NCCL communicator: payloads move by "
+                            "copy engine over CUDA IPC peer memory, flags by cuStreamWrite/WaitValue64)"},
         "per_gpu_updates_per_s": value / n_ranks,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": None, "peak_source": peak_kind,
-                     "kernel": "k_accumulate*", "bytes_per_launch": alg_bytes},
+                     "frac": achieved / peak,
+                     "traffic": k1_traffic(lib, n, p_local, B * lanes, args.dtype, args.arith),
+                     "peak_source": peak_kind, "kernel": "k_accumulate*", "bytes_per_launch": alg_bytes,
+                     "walkers_per_launch": B * lanes, "planes_per_launch": p_local},
         "nvlink": {"bytes_per_step_per_gpu": ring_bytes,
                    "wire": "payload cores" if eng_wire_cores else "staged payloads",
                    "achieved_gbs": ring_bytes / (ms * 1e-3) / 1e9, "peak_gbs": 770.0,
-                   "peak_source": "B200_PROFILING.md measured peer copy"},
+                   "peak_source": "B200_PROFILING.md measured peer copy",
+                   "achieved_note": "wire bytes / step time (computed); measured counters per rank below",
+                   "measured_per_rank": [x["nvlink"] for x in stats]},
         "clocks": stats[0]["clk"],
+        "clocks_per_rank": [x["clk"] for x in stats],
         "e2e": e2e,
         "host": {"enqueue_ms_per_step": max(x["host_ms"] for x in stats),
                  "native_rounds": eng_native,
@@ -744,6 +808,58 @@ def run_ring(args):
         "gpu_launches": args.steps * S,  # K1 launches per rank per step = S (own + S-1 received)
     }
     print(json.dumps(line), flush=True)
+
+
+class NvlinkCounters:
+    """NVLink data bytes this GPU sent and received during the timed region,
+    from NVML's throughput counters (nvmlDeviceGetFieldValues,
+    NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX/RX, KiB, summed over links), read
+    before and after.  On a GPU without active NVLinks (or a driver that does
+    not expose the fields) the result says so instead of a number."""
+
+    TX, RX = 138, 139  # NVML_FI_DEV_NVLINK_THROUGHPUT_DATA_TX / _RX
+
+    def __init__(self, gpu_index: int):
+        self.err = None
+        self.h = None
+        self.a = self.b = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(gpu_index)
+        except Exception as exc:  # NVML absent
+            self.err = f"nvml unavailable: {exc}"
+
+    def _read(self):
+        vals = self.nvml.nvmlDeviceGetFieldValues(self.h, [self.TX, self.RX])
+        out = []
+        for v in vals:
+            if v.nvmlReturn != 0:
+                raise RuntimeError(f"field {v.fieldId}: nvml return {v.nvmlReturn}")
+            out.append(int(v.value.ullVal) * 1024)
+        return out
+
+    def start(self):
+        if self.h is not None:
+            try:
+                self.a = self._read()
+            except Exception as exc:
+                self.err = str(exc)
+
+    def stop(self):
+        if self.h is not None and self.a is not None:
+            try:
+                self.b = self._read()
+            except Exception as exc:
+                self.err = str(exc)
+
+    def result(self, steps: int) -> dict:
+        if self.a is None or self.b is None:
+            return {"source": "nvml", "unavailable": self.err or "not read"}
+        tx, rx = self.b[0] - self.a[0], self.b[1] - self.a[1]
+        return {"source": "nvml NVLINK_THROUGHPUT_DATA_TX/RX", "tx_bytes_per_step": tx / steps,
+                "rx_bytes_per_step": rx / steps}
 
 
 def ring_model_line(n, planes, gpus, batch, dtype, subring_size, lanes):
@@ -836,6 +952,8 @@ def main():
     ap.add_argument("--planes", type=int, default=0, help="override the exchange-plane count (N=1)")
     ap.add_argument("--max-g4", action="store_true", help="allocate + update + verify the largest N=4608 slice")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--skip-extras", action="store_true",
+                    help="lab runs: headline + parity check only (no e2e, sweeps, other configs)")
     ap.add_argument("--subring-size", type=int, default=0, help="ring size S for N > 1 (default N; c3: 4)")
     ap.add_argument("--lanes", type=int, default=0, help="walker streams per GPU for N > 1 (default 1; c3: 2)")
     args = ap.parse_args()

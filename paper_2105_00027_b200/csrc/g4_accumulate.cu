@@ -796,7 +796,9 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 25: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2, 1, 1, 1>, FUSED, 2>(prm, st);
         case 27: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4, 1, 1, 1>, FUSED, 3>(prm, st);
         case 40:
-        case 42:  // v3, the persistent kernel: fused + deferred, complex128 slices only
+        case 42:
+        case 43:
+        case 44:  // v3, the persistent kernel: fused + deferred, complex128 slices only
             if constexpr (FUSED && sizeof(R) == 8)
                 return launch_pst<RG>(g, prm.g4, prm.lo, prm.hi, prm.n,
                                       reinterpret_cast<const void* const*>(prm.stg), prm.nbatch, st);
@@ -833,7 +835,9 @@ static bool geom_info(int g, GeomInfo* out) {
         case 25: *out = info_of<V2Geom<double, 8, 2, 3, 4, 2, 1, 1, 1>>(2); return true;
         case 27: *out = info_of<V2Geom<double, 8, 1, 2, 2, 4, 1, 1, 1>>(3); return true;
         case 40:
-        case 42: {
+        case 42:
+        case 43:
+        case 44: {
             int pp, dd, q, dr, nst;
             pst_geom_info(g, &pp, &dd, &q, &dr, &nst);
             *out = {pp, dd, q, dr, nst, 1, 16};

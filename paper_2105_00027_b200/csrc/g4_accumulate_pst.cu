@@ -503,13 +503,15 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
 // v3 geometries (id >= 40 in the G4RING_V2GEOM numbering):
 //   40: 8x4 blocks, 2x4 warps (tile 16 planes x 16 diagonals), 4 stages, 4 park slots
 //   (a 32 x 8 tile, 4x2 warps, needs a band of 39 rows + 32 columns: beyond the staged halo)
-//   42: as 40 with 3 stages and 8 park slots
+//   42: as 40 with 3 stages and 8 park slots; 43: 3 stages, 10 park slots; 44: 2 stages, 16 park slots
 template <typename RG>
 g4_status launch_pst(int geom, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                      int32_t nbatch, cudaStream_t st) {
     switch (geom) {
         case 40: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 4, 4>>(g4p, lo, hi, n, staged, nbatch, st);
         case 42: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 3, 8>>(g4p, lo, hi, n, staged, nbatch, st);
+        case 43: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 3, 10>>(g4p, lo, hi, n, staged, nbatch, st);
+        case 44: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 2, 16>>(g4p, lo, hi, n, staged, nbatch, st);
         default: return fail(G4_ERR_CONTRACT, "unknown v3 geometry");
     }
 }
@@ -522,6 +524,8 @@ bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst) {
     switch (geom) {
         case 40: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 4; return true;
         case 42: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 3; return true;
+        case 43: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 3; return true;
+        case 44: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 2; return true;
         default: return false;
     }
 }

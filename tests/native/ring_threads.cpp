@@ -82,6 +82,13 @@ static int32_t allgather(void* ctx, int32_t group, const void* send, int64_t byt
     } while (0)
 
 int main(int argc, char** argv) {
+    // Several ranks (threads) share one CUDA context here, each with a compute
+    // stream, its comm streams and a copy stream; the flag waits are stream
+    // memops that block their hardware queue.  With more streams than queues
+    // (CUDA_DEVICE_MAX_CONNECTIONS, default 8) two ranks' streams can share a
+    // queue, and a wait at its head holds back the other rank's work that would
+    // satisfy it.  One queue per stream: set before the context exists.
+    setenv("CUDA_DEVICE_MAX_CONNECTIONS", "32", 0);
     const int world = argc > 1 ? std::atoi(argv[1]) : 4;
     const int S = argc > 2 ? std::atoi(argv[2]) : 2;
     const int lanes = argc > 3 ? std::atoi(argv[3]) : 2;
@@ -118,6 +125,20 @@ int main(int argc, char** argv) {
     std::vector<std::vector<double>> result(S);  // sub-ring 0 slices after the reduce
     std::vector<int64_t> los(S), his(S);
 
+    // host-fed inputs: per rank, rounds x (batch x lanes) reference-layout walkers
+    std::vector<std::vector<void*>> ups(world), downs(world);
+    if (fed)
+        for (int r = 0; r < world; ++r) {
+            cudaSetDevice(r % ngpu);
+            for (int i = 0; i < batch * lanes * rounds; ++i) {
+                void *u, *d;
+                cudaMalloc(&u, (size_t)n * n * 16);
+                cudaMalloc(&d, (size_t)n * n * 16);
+                ups[r].push_back(u);
+                downs[r].push_back(d);
+            }
+        }
+
     std::vector<std::thread> threads;
     for (int r = 0; r < world; ++r) {
         threads.emplace_back([&, r] {
@@ -132,13 +153,16 @@ int main(int argc, char** argv) {
                 // batch-major, lanes in order), rank 0 late on every round; no wait
                 // between rounds, so the other ranks stage round m + 1 while their
                 // comm streams still wait for rank 0 to take round m
+                // Device inputs are allocated before the ring starts and freed after
+                // every thread has joined (main): cudaFree synchronises the device,
+                // and the other ranks' streams sit in flag waits on rank 0 until it
+                // stages.  Copies go through a non-blocking stream of this thread.
                 const int cnt = batch * lanes;
                 std::vector<double> hu((size_t)n * n * 2), hd((size_t)n * n * 2);
-                std::vector<void*> du((size_t)cnt * rounds), dd((size_t)cnt * rounds);
-                for (size_t i = 0; i < du.size(); ++i) {
-                    cudaMalloc(&du[i], hu.size() * 8);
-                    cudaMalloc(&dd[i], hd.size() * 8);
-                }
+                std::vector<void*>& du = ups[r];
+                std::vector<void*>& dd = downs[r];
+                cudaStream_t cp;
+                cudaStreamCreateWithFlags(&cp, cudaStreamNonBlocking);
                 for (int m = 0; m < rounds; ++m) {
                     if (r == 0 && delay_ms) std::this_thread::sleep_for(std::chrono::milliseconds(delay_ms));
                     for (int b = 0; b < batch; ++b)
@@ -146,18 +170,16 @@ int main(int argc, char** argv) {
                             g4o_fill_gsigma(cfg.seed, r, t, (int64_t)m * batch + b, n, G4_MODE_INTEGER, hu.data(),
                                             hd.data());
                             const size_t i = (size_t)m * cnt + b * lanes + t;  // per-round buffers
-                            cudaMemcpy(du[i], hu.data(), hu.size() * 8, cudaMemcpyHostToDevice);
-                            cudaMemcpy(dd[i], hd.data(), hd.size() * 8, cudaMemcpyHostToDevice);
+                            cudaMemcpyAsync(du[i], hu.data(), hu.size() * 8, cudaMemcpyHostToDevice, cp);
+                            cudaMemcpyAsync(dd[i], hd.data(), hd.size() * 8, cudaMemcpyHostToDevice, cp);
+                            cudaStreamSynchronize(cp);
                         }
                     CHECK(g4_ring_stage(ring, du.data() + (size_t)m * cnt, dd.data() + (size_t)m * cnt, cnt,
                                         G4_C128));
                     CHECK(g4_ring_measure(ring, m, 0));
                 }
                 CHECK(g4_ring_wait(ring, 60000));
-                for (size_t i = 0; i < du.size(); ++i) {
-                    cudaFree(du[i]);
-                    cudaFree(dd[i]);
-                }
+                cudaStreamDestroy(cp);
             }
             CHECK(g4_ring_wait(ring, 60000));
             CHECK(g4_ring_reduce(ring));
@@ -174,6 +196,11 @@ int main(int argc, char** argv) {
         });
     }
     for (auto& t : threads) t.join();
+    for (int r = 0; r < world; ++r)
+        for (size_t i = 0; i < ups[r].size(); ++i) {
+            cudaFree(ups[r][i]);
+            cudaFree(downs[r][i]);
+        }
 
     // oracle: every walker (world rank, lane, measurement) applied to all N planes
     std::vector<double> ref((size_t)n * n * n * 2, 0.0), up((size_t)n * n * 2), down((size_t)n * n * 2);
