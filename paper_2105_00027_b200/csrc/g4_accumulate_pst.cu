@@ -54,7 +54,8 @@ struct V3Geom {
     static constexpr uint32_t PARK_OFF = NST * STAGE_BYTES;
     static constexpr uint32_t PARK_BYTES = 4 * NPARK * CHUNK_BYTES;
     static constexpr uint32_t BAR_OFF = PARK_OFF + PARK_BYTES;
-    static constexpr size_t SMEM = BAR_OFF + (2 * NST + 4) * sizeof(uint64_t) + 16;
+    // barriers: full/empty per stage, tfull/tready x 2, the TMEM slot (8 B), one per park slot
+    static constexpr size_t SMEM = BAR_OFF + (2 * NST + 5 + 4 * NPARK) * sizeof(uint64_t) + 16;
     static constexpr int BLOCK_COLS = PP * DD * 4;          // TMEM columns per consumer warp block
     // the last tile's blocks (CW x PP chunks) fit the idle stage buffers: consumers write it back
     static constexpr bool LAST_DIRECT = (size_t)CW * PP * CHUNK_BYTES <= (size_t)NST * STAGE_BYTES;
@@ -122,6 +123,16 @@ __device__ __forceinline__ void pst_edge_chunk(const TmaParams<double>& P, int p
         if (run1 < cnt) segment_out<true, double>(row, park + d * 32 + run1, cnt - run1);
     }
 }
+// Lab timeline (G4RING_V3_TRACE): row 31 of a CTA's trace holds %globaltimer
+// stamps (ns, comparable across SMs): 0 CTA entry, 1 first payload landed,
+// 2 consumers done, 3 epilogue done, 4 producer done.
+__device__ __forceinline__ void trace_gt(long long* tr, int slot) {
+    if (tr) {
+        long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        tr[((size_t)blockIdx.x * 32 + 31) * 8 + slot] = t;
+    }
+}
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -135,8 +146,176 @@ struct V3Tile {
 template <class G>
 __device__ __forceinline__ V3Tile v3_tile(const TmaParams<double>& P, int lin) {
     const int n = P.n;
-    const TileCoord tc = tile_coord((unsigned)lin, P.nx, (n + 31) / 32, (n + G::DR - 1) / G::DR);
+    const int ny = (n + 31) / 32, nz = (n + G::DR - 1) / G::DR;
+    if (P.hints & 4096) {  // lab: plane chunks slowest (each wave walks rows/columns of one chunk)
+        const int x = lin / (ny * nz), r = lin % (ny * nz);
+        const TileCoord tc = tile_coord((unsigned)r, 1, ny, nz);
+        return {P.lo + (int64_t)x * G::Q, tc.z * G::DR, tc.y * 32};
+    }
+    // lab: block shape of the L2-aware walk (hints 32768: 8 row groups, 65536: 4 column chunks)
+    const int tbz = (P.hints & 32768) ? 8 : TILE_BZ, tby = (P.hints & 65536) ? 4 : TILE_BY;
+    const TileCoord tc = tile_coord((unsigned)lin, P.nx, ny, nz, tby, tbz);
     return {P.lo + (int64_t)tc.x * G::Q, tc.z * G::DR, tc.y * 32};
+}
+// The CTA's tiles: CTA c takes tiles c, c + grid, ... (default), or (lab, hint
+// 8192) one contiguous run of the tile order.
+__device__ __forceinline__ int v3_count(const TmaParams<double>& P, int ntiles) {
+    const int b = (int)blockIdx.x, g = (int)gridDim.x;
+    if (P.hints & 8192) {
+        const int per = (ntiles + g - 1) / g;
+        return max(0, min(ntiles, (b + 1) * per) - b * per);
+    }
+    return b < ntiles ? (ntiles - 1 - b) / g + 1 : 0;
+}
+__device__ __forceinline__ int v3_lin(const TmaParams<double>& P, int ntiles, int k) {
+    const int b = (int)blockIdx.x, g = (int)gridDim.x;
+    if (P.hints & 8192) return b * ((ntiles + g - 1) / g) + k;
+    return b + k * g;
+}
+
+// Lab (hint 16384): epilogue warp q pulls the G4 lines of its two blocks of
+// tile t into L2 through the LSU (prefetch.global.L2; the TMA queue stays free
+// for the fills), so the tile's reduces later hit in L2.
+template <class G>
+__device__ __forceinline__ void v3_prefetch_g4(const TmaParams<double>& P, const V3Tile& t, int q, int lane) {
+    constexpr int PP = G::PP, DD = G::DD, PTS = 5;  // 5 points cover a 512-B row segment's lines
+    const int n = P.n;
+#pragma unroll 1
+    for (int i = lane; i < 2 * PP * DD * PTS; i += 32) {
+        const int pt = i % PTS, row = (i / PTS) % DD, pl = (i / (PTS * DD)) % PP, h = i / (PTS * DD * PP);
+        const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
+        const int plane = (int)(t.q0 - P.lo) + PP * wq + pl;
+        const int k1 = t.k1_0 + DD * wr + row;
+        if (plane >= (int)(P.hi - P.lo) || k1 >= n) continue;
+        int k2 = t.j0 + DD * wr + row + (pt == 4 ? 31 : 8 * pt);
+        while (k2 >= n) k2 -= n;
+        const Cx<double>* a = P.g4 + ((int64_t)plane * n + k1) * n + k2;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
+    }
+}
+
+// The load/add/store epilogue (hint 131072): instead of adding each parked
+// chunk into the slice with an L2 reduction (RMW inside L2, measured to cap at
+// 5.3 TB/s on its own, tools/rmw_bench.cu), the warp loads the chunk's G4 rows
+// into its park slot by TMA ahead of time (NPARK - 2 chunks ahead, across tile
+// boundaries, so the next tile's first loads overlap the consumers' compute),
+// adds its TMEM values and stores the chunk back by TMA (6.5 TB/s alone).  The
+// sum per entry is the same IEEE add as the L2 reduction's, so results are
+// bitwise those of the reduce path.  Edge chunks (row wrap, last column strip)
+// keep the reduce path.
+template <class G>
+__device__ __forceinline__ void epilogue_ls(const TmaParams<double>& P, int ntiles, int my_tiles, int q, int lane,
+                                            uint32_t tq, uint64_t* tfull, uint64_t* tready, uint64_t* pbar,
+                                            uint32_t park, unsigned char* smem_raw) {
+    constexpr int PP = G::PP, DD = G::DD, NPARK = G::NPARK, LA = NPARK - 2;
+    static_assert(DD == 4, "one 16-column TMEM load per chunk");
+    const int n = P.n;
+    const uint64_t gmap = reinterpret_cast<uint64_t>(&P.gmap);
+    const int drained = (!G::LAST_DIRECT || (P.hints & 1024)) ? my_tiles : my_tiles - 1;
+    // chunk c of a tile: block h = c / np (consumer warp q + 4h), plane p = c % np
+    struct Ck {
+        int plane, k1b, c0, j0e, j0;
+        bool box;
+        uint32_t col;  // TMEM column offset of the chunk in its buffer
+    };
+    auto chunk = [&](const V3Tile& t, int c, int np) {
+        const int h = c / np, p = c % np;
+        const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
+        const int e0 = DD * wr;
+        Ck k;
+        k.plane = (int)(t.q0 - P.lo) + PP * wq + p;
+        k.k1b = t.k1_0 + e0;
+        k.c0 = 2 * (t.j0 - t.k1_0 + n);
+        k.j0e = t.j0 + e0;
+        k.j0 = t.j0;
+        k.box = P.use_gmap && k.k1b + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n;
+        k.col = (uint32_t)(h * G::BLOCK_COLS + p * 16);
+        return k;
+    };
+    auto planes_of = [&](const V3Tile& t) { return min(PP, (int)(P.hi - P.lo) - ((int)(t.q0 - P.lo) + PP * (q % G::CWQ))); };
+    // load cursor: tile lk, chunk lc, sequence lseq
+    int lk = 0, lc = 0, lseq = 0;
+    V3Tile lt = v3_tile<G>(P, v3_lin(P, ntiles, 0));
+    int lnp = drained > 0 ? planes_of(lt) : 0;
+    auto issue_load = [&]() {
+        if (lk >= drained) return;
+        const Ck k = chunk(lt, lc, lnp);
+        const int slot = lseq % NPARK;
+        if (lane == 0) {
+            if (k.box) {
+                mbar_arrive_expect_tx(&pbar[slot], G::CHUNK_BYTES);
+                asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                             " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(park + slot * G::CHUNK_BYTES), "l"(gmap),
+                             "r"(k.c0), "r"(k.k1b), "r"(k.plane), "r"(smem_u32(&pbar[slot]))
+                             : "memory");
+            } else {
+                mbar_arrive(&pbar[slot]);  // no load: the phase completes at once
+            }
+        }
+        ++lseq;
+        if (++lc == 2 * lnp) {
+            lc = 0;
+            if (++lk < drained) {
+                lt = v3_tile<G>(P, v3_lin(P, ntiles, lk));
+                lnp = planes_of(lt);
+            }
+        }
+    };
+    for (int i = 0; i < LA; ++i) issue_load();
+    int seq = 0;
+    for (int k = 0; k < drained; ++k) {
+        const int b = k & 1;
+        mbar_wait(&tfull[b], (k >> 1) & 1);
+        tc_fence_after();
+        if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
+        const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
+        const int np = planes_of(t);
+#pragma unroll 1
+        for (int c = 0; c < 2 * np; ++c, ++seq) {
+            const Ck k2 = chunk(t, c, np);
+            const int slot = seq % NPARK;
+            const uint32_t sa = park + slot * G::CHUNK_BYTES + lane * 16;
+            uint32_t v[16];
+            tmem_ld16(tq + b * 256 + k2.col, v);
+            mbar_wait(&pbar[slot], (seq / NPARK) & 1);
+            tmem_wait_ld();
+            if (k2.box) {
+#pragma unroll
+                for (int d = 0; d < DD; ++d) {
+                    double gr, gi;
+                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(gr), "=d"(gi) : "r"(sa + d * 512) : "memory");
+                    gr = __dadd_rn(gr, __hiloint2double((int)v[4 * d + 1], (int)v[4 * d]));
+                    gi = __dadd_rn(gi, __hiloint2double((int)v[4 * d + 3], (int)v[4 * d + 2]));
+                    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(sa + d * 512), "d"(gr), "d"(gi) : "memory");
+                }
+            } else {
+#pragma unroll
+                for (int d = 0; d < DD; ++d)
+                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sa + d * 512), "r"(v[4 * d]),
+                                 "r"(v[4 * d + 1]), "r"(v[4 * d + 2]), "r"(v[4 * d + 3]) : "memory");
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
+            __syncwarp();
+            if (lane == 0) {
+                const uint32_t sp = park + slot * G::CHUNK_BYTES;
+                if (k2.box)
+                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
+                                 ::"l"(gmap), "r"(sp), "r"(k2.c0), "r"(k2.k1b), "r"(k2.plane) : "memory");
+                else
+                    pst_edge_chunk(P, k2.plane, k2.k1b, k2.j0e, k2.j0, DD,
+                                   reinterpret_cast<const Cx<double>*>(smem_raw + (sp - smem_u32(smem_raw))));
+                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                // the slot LA chunks ahead was last used by chunk seq - 2: its store has read it
+                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+            }
+            __syncwarp();
+            issue_load();
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 1 + 6 * (q == 3)] = clock64();
+        if (lane == 0) mbar_arrive(&tready[b]);
+    }
 }
 
 template <typename RG, class G>
@@ -150,14 +329,16 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     uint64_t* tfull = empty + NST;  // [2] consumers -> epilogue: the tile's blocks are in TMEM buffer b
     uint64_t* tready = tfull + 2;   // [2] epilogue -> consumers: TMEM buffer b has been drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 2);
+    uint64_t* pbar = tready + 3;    // [4][NPARK] G4 chunk loads into the park slots (load/add/store epilogue)
 
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = P.nx * ((n + 31) / 32) * ((n + DR - 1) / DR);
-    const int my_tiles = (int)blockIdx.x < ntiles ? (ntiles - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    const int my_tiles = v3_count(P, ntiles);
     const int nb = P.nbatch;
 
     if (threadIdx.x == 0) {
+        trace_gt(P.trace, 0);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], G::CW);
@@ -166,6 +347,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             mbar_init(&tfull[b], G::CW);
             mbar_init(&tready[b], 4);
         }
+        for (int i = 0; i < 4 * G::NPARK; ++i) mbar_init(&pbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 8) {  // the whole of TMEM (one CTA per SM)
@@ -185,7 +367,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             const uint64_t keep = l2_policy_evict_last();  // payload rows are re-read by many tiles
             int it = 0;
             for (int k = 0; k < my_tiles; ++k) {
-                const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
+                const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
                 const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
                 const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
                 const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
@@ -207,6 +389,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                     }
                 }
             }
+            trace_gt(P.trace, 4);
         }
         __syncwarp();
         return;
@@ -222,16 +405,21 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
         const uint64_t gmap = reinterpret_cast<uint64_t>(&P.gmap);
         const uint64_t stream = l2_policy_evict_first();  // slice lines are touched once per pass
+        if (P.hints & 131072) {
+            epilogue_ls<G>(P, ntiles, my_tiles, q, lane, tq, tfull, tready, pbar + q * G::NPARK,
+                           smem_u32(smem_raw + G::PARK_OFF) + (uint32_t)q * G::NPARK * G::CHUNK_BYTES, smem_raw);
+        } else {
         int pair = 0;  // chunk pairs parked by this warp (slot = pair % NSLOT)
         constexpr int NSLOT = G::NPARK / 2;
         const int drained = (!G::LAST_DIRECT || (P.hints & 1024)) ? my_tiles : my_tiles - 1;  // see consumers
         for (int k = 0; k < drained && !(P.hints & 256); ++k) {
             const int b = k & 1;
+            if (P.hints & 16384) v3_prefetch_g4<G>(P, v3_tile<G>(P, v3_lin(P, ntiles, k)), q, lane);
             if (P.hints & 64) mbar_wait_sleep(&tfull[b], (k >> 1) & 1);
             else mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
-            if (P.trace && k < 32 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
-            const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
+            if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
+            const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
@@ -282,10 +470,12 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             tc_fence_before();
             __syncwarp();
-            if (P.trace && k < 32 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 1 + 6 * (q == 3)] = clock64();
+            if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 1 + 6 * (q == 3)] = clock64();
             if (lane == 0) mbar_arrive(&tready[b]);
         }
+        }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        if (warp == 8 && lane == 0) trace_gt(P.trace, 3);
         __syncwarp();
         // every epilogue warp is past its last tcgen05.ld: release TMEM
         asm volatile("barrier.sync 1, 128;" ::: "memory");
@@ -305,7 +495,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     int pend = -1;  // TMEM buffer whose stores are issued but not yet announced (tfull)
     const bool defer_st = !(P.hints & 2048);
     for (int k = 0; k < my_tiles; ++k) {
-        const V3Tile t = v3_tile<G>(P, (int)blockIdx.x + k * (int)gridDim.x);
+        const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
         int ps = 0, pd = 0;
         if constexpr (G::ES == 8) {
             const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
@@ -315,7 +505,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         }
         const int sh_o = (PP * wq + DR - DD - e0) * G::W + (31 - lane) + ps;  // band row of (p, d): + j * W
         const int dr_o = e0 * G::W + lane + pd;                                // direct row d: + d * W
-        if (P.trace && k < 32 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 4] = clock64();
+        if (P.trace && k < 31 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 4] = clock64();
         Cx<R> acc[PP][DD];
 #pragma unroll
         for (int p = 0; p < PP; ++p)
@@ -325,6 +515,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         for (int w = 0; w < nb; ++w, ++it) {
             const int s = it % NST;
             if (!(P.hints & 32)) mbar_wait(&full[s], (it / NST) & 1);  // 32: lab only (no fills at all)
+            if (it == 0 && warp == 0 && lane == 0) trace_gt(P.trace, 1);
             const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
             const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
             const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
@@ -400,6 +591,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // park read before exit
             }
             __syncwarp();
+            if (warp == 0 && lane == 0) trace_gt(P.trace, 2);
             break;
         }
         // hand the block to the epilogue through TMEM buffer b
@@ -409,7 +601,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             if (P.hints & 64) mbar_wait_sleep(&tready[b], ((k >> 1) - 1) & 1);
             else mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
         }
-        if (P.trace && k < 32 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 3] = clock64() - tw0;
+        if (P.trace && k < 31 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 3] = clock64() - tw0;
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < PP * DD / 8; ++c) {  // 8 entries (32 columns) per store
@@ -424,7 +616,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             tmem_st32(tq + b * 256 + c * 32, v);
         }
-        if (P.trace && k < 32 && lane == 0 && (warp == 0 || warp == 7))
+        if (P.trace && k < 31 && lane == 0 && (warp == 0 || warp == 7))
             P.trace[((size_t)blockIdx.x * 32 + k) * 8 + (warp == 0 ? 2 : 5)] = clock64();
         pend = b;  // announced after the next tile's first walker (or below)
         if (!defer_st || k == my_tiles - 1) {

@@ -34,20 +34,21 @@ struct TileCoord {
     int x, y, z;
 };
 
-__device__ __forceinline__ TileCoord tile_coord(unsigned lin, int nx, int ny, int nz) {
-    const unsigned per_row = (unsigned)nx * ny * TILE_BZ;  // CTAs in a full block row
+__device__ __forceinline__ TileCoord tile_coord(unsigned lin, int nx, int ny, int nz, int tby = TILE_BY,
+                                                int tbz = TILE_BZ) {
+    const unsigned per_row = (unsigned)nx * ny * tbz;  // CTAs in a full block row
     const int br = (int)(lin / per_row);
     unsigned r = lin - (unsigned)br * per_row;
-    const int bze = min(TILE_BZ, nz - br * TILE_BZ);
-    const unsigned per_blk = (unsigned)nx * TILE_BY * bze;
+    const int bze = min(tbz, nz - br * tbz);
+    const unsigned per_blk = (unsigned)nx * tby * bze;
     const int by = (int)(r / per_blk);
     r -= (unsigned)by * per_blk;
-    const int bye = min(TILE_BY, ny - by * TILE_BY);
+    const int bye = min(tby, ny - by * tby);
     TileCoord t;
     t.x = (int)(r % nx);
     r /= nx;
-    t.y = by * TILE_BY + (int)(r % bye);
-    t.z = br * TILE_BZ + (int)(r / bye);
+    t.y = by * tby + (int)(r % bye);
+    t.z = br * tbz + (int)(r / bye);
     return t;
 }
 
@@ -182,6 +183,8 @@ struct alignas(64) TmaParams {
     int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS, measurement only): 1/2 L2 evict_first/last hints,
                     // 16 no slice write-back, 32 no payload fills, 64 sleeping waits, 128 no stage release,
                     // 256 no TMEM hand-off, 1024 last tile via TMEM, 2048 TMEM-store wait not deferred
+                    // (an L2 prefetch of the tile's G4 block, by TMA at the tile's start, measured
+                    // 6-130 % slower, lab r02e: removed)
     long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
 };
 

@@ -41,7 +41,8 @@ def main():
     torch.cuda.synchronize()
     raw = np.fromfile(path, dtype=np.int64)
     grid = raw.size // (a.passes * 32 * 8)
-    tr = raw.reshape(a.passes, grid, 32, 8)[-1]  # last pass
+    tr = raw.reshape(a.passes, grid, 32, 8)[-1].copy()  # last pass
+    tr[:, 31, :] = 0  # row 31: globaltimer stamps (below)
     # [0] epi q0 tfull done, [1] epi q0 drained, [2] cons w0 tile done, [3] cons w0 tready wait,
     # [4] cons w0 tile start, [5] cons w7 tile done, [6] epi q3 tfull done, [7] epi q3 drained
     ok = tr[:, :, 4] > 0
@@ -71,6 +72,16 @@ def main():
     print(f"epilogue drain q0 (tfull -> tready):  {pct(drain)}")
     print(f"epilogue drain q3:                    {pct(drain3)}")
     print(f"consumer w0 tready wait:             {pct(wait)}  (nonzero in {np.mean(wait > 200) * 100:.0f}% of tiles)")
+    g = raw.reshape(a.passes, grid, 32, 8)[-1][:, 31, :5].astype(np.float64)  # globaltimer ns
+    t0 = g[:, 0].min()
+    us = lambda x: f"median {np.median(x):7.2f}  min {np.min(x):7.2f}  max {np.max(x):7.2f} us"
+    print("globaltimer (us from the first CTA entry):")
+    print(f"  CTA entry:                 {us((g[:, 0] - t0) / 1e3)}")
+    print(f"  first payload landed:      {us((g[:, 1] - g[:, 0]) / 1e3)}  (after its CTA entry)")
+    print(f"  consumers done:            {us((g[:, 2] - t0) / 1e3)}")
+    print(f"  epilogue done:             {us((g[:, 3] - t0) / 1e3)}")
+    print(f"  producer done:             {us((g[:, 4] - t0) / 1e3)}")
+    print(f"  kernel span (entry->last done): {(max(g[:, 2].max(), g[:, 3].max()) - t0) / 1e3:.2f} us")
     os.unlink(path)
 
 
