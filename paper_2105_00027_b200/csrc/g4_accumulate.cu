@@ -852,7 +852,7 @@ static bool geom_info(int g, GeomInfo* out) {
 // not read at CTA start (K1_DEFER), the 2-CTA/SM, 32-entry-register-block
 // geometry 12 beats 13 (lab24: -7 % at B = 16, -10 % at N = 4608).
 // G4RING_V2GEOM overrides.
-static int v2_geom(int64_t planes, bool deferred, bool c64_slice) {
+static int v2_geom(int n, int64_t planes, bool deferred, bool c64_slice, int nbatch) {
     static int forced = -2;
     if (forced == -2) {
         const char* e = getenv("G4RING_V2GEOM");
@@ -861,10 +861,17 @@ static int v2_geom(int64_t planes, bool deferred, bool c64_slice) {
     if (forced >= 0) return forced;
     if (planes < 16) return 19;
     if (!deferred) return 13;
-    // complex128 slices: the persistent TMEM-handoff kernel (v3, geometry 40):
-    // 141.7 us at B = 8 against 161.6 for geometry 25 (profiles/r02_summary.md).
-    // complex64 slices keep geometry 12 (the producer warp group loses there, lab35).
-    return c64_slice ? 12 : 40;
+    // complex128 slices: the persistent TMEM-handoff kernel (v3).  Geometry 40
+    // (4 stages, 4 park slots) at N <= 1024; at N = 4608 the slice reduces miss
+    // L2 far more and geometry 43 (3 stages, 10 park slots) wins, 13.9 ms vs
+    // 19.6 per pass of config 4's share (lab r02c).  complex64 slices keep
+    // geometry 12 (the producer warp group loses there, lab35).
+    // With few walkers per pass the persistent kernel's fixed hand-off and
+    // slice reduction per tile dominate: geometry 25 below V3_MIN_WALKERS.
+    if (c64_slice) return 12;
+    static const int v3_min = env_int("G4RING_V3_MIN_WALKERS", 6);
+    if (nbatch < v3_min) return 25;
+    return n > 2048 ? 43 : 40;
 }
 
 static bool use_v2(int n, int64_t planes) {
@@ -877,7 +884,9 @@ static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     if (use_v2(prm.n, planes))
         return launch_v2_geom<R, RG, FUSED>(
-            v2_geom(planes, FUSED && defer_update(prm.nbatch, planes), sizeof(R) == 4), prm, st);
+            v2_geom(prm.n, planes, FUSED && defer_update(prm.nbatch, planes), sizeof(R) == 4,
+                    std::min<int32_t>(prm.nbatch, TMA_MAXW)),
+            prm, st);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
@@ -959,9 +968,8 @@ g4_status g4_k1_config(int32_t n, int64_t planes, int32_t nbatch, int32_t dtype,
     if (use_v2(n, planes)) {
         const bool deferred = g_arith == G4_ARITH_FUSED && defer_update(walkers, planes);
         GeomInfo gi;
-        if (!geom_info(v2_geom(planes, deferred, dtype == G4_C64), &gi))
-            return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
-        const int g = v2_geom(planes, deferred, dtype == G4_C64);
+        const int g = v2_geom(n, planes, deferred, dtype == G4_C64, walkers);
+        if (!geom_info(g, &gi)) return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
         const int32_t v[9] = {g >= 40 ? 3 : 2, gi.pp, gi.dd, gi.q, gi.dr, gi.nst, gi.ctas, gi.warps, deferred ? 1 : 0};
         std::memcpy(out, v, sizeof(v));
     } else {

@@ -54,8 +54,8 @@ struct V3Geom {
     static constexpr uint32_t PARK_OFF = NST * STAGE_BYTES;
     static constexpr uint32_t PARK_BYTES = 4 * NPARK * CHUNK_BYTES;
     static constexpr uint32_t BAR_OFF = PARK_OFF + PARK_BYTES;
-    // barriers: full/empty per stage, tfull/tready x 2, the TMEM slot (8 B), one per park slot
-    static constexpr size_t SMEM = BAR_OFF + (2 * NST + 5 + 4 * NPARK) * sizeof(uint64_t) + 16;
+    // barriers (full/empty per stage, tfull/tready x 2), then the TMEM address and the tile ids
+    static constexpr size_t SMEM = BAR_OFF + (2 * NST + 4) * sizeof(uint64_t) + 8 + (NST + 2) * sizeof(int) + 8;
     static constexpr int BLOCK_COLS = PP * DD * 4;          // TMEM columns per consumer warp block
     // the last tile's blocks (CW x PP chunks) fit the idle stage buffers: consumers write it back
     static constexpr bool LAST_DIRECT = (size_t)CW * PP * CHUNK_BYTES <= (size_t)NST * STAGE_BYTES;
@@ -146,177 +146,24 @@ struct V3Tile {
 template <class G>
 __device__ __forceinline__ V3Tile v3_tile(const TmaParams<double>& P, int lin) {
     const int n = P.n;
-    const int ny = (n + 31) / 32, nz = (n + G::DR - 1) / G::DR;
-    if (P.hints & 4096) {  // lab: plane chunks slowest (each wave walks rows/columns of one chunk)
-        const int x = lin / (ny * nz), r = lin % (ny * nz);
-        const TileCoord tc = tile_coord((unsigned)r, 1, ny, nz);
-        return {P.lo + (int64_t)x * G::Q, tc.z * G::DR, tc.y * 32};
-    }
-    // lab: block shape of the L2-aware walk (hints 32768: 8 row groups, 65536: 4 column chunks)
-    const int tbz = (P.hints & 32768) ? 8 : TILE_BZ, tby = (P.hints & 65536) ? 4 : TILE_BY;
-    const TileCoord tc = tile_coord((unsigned)lin, P.nx, ny, nz, tby, tbz);
+    const TileCoord tc = tile_coord((unsigned)lin, P.nx, (n + 31) / 32, (n + G::DR - 1) / G::DR);
     return {P.lo + (int64_t)tc.x * G::Q, tc.z * G::DR, tc.y * 32};
 }
-// The CTA's tiles: CTA c takes tiles c, c + grid, ... (default), or (lab, hint
-// 8192) one contiguous run of the tile order.
-__device__ __forceinline__ int v3_count(const TmaParams<double>& P, int ntiles) {
-    const int b = (int)blockIdx.x, g = (int)gridDim.x;
-    if (P.hints & 8192) {
-        const int per = (ntiles + g - 1) / g;
-        return max(0, min(ntiles, (b + 1) * per) - b * per);
-    }
-    return b < ntiles ? (ntiles - 1 - b) / g + 1 : 0;
-}
-__device__ __forceinline__ int v3_lin(const TmaParams<double>& P, int ntiles, int k) {
-    const int b = (int)blockIdx.x, g = (int)gridDim.x;
-    if (P.hints & 8192) return b * ((ntiles + g - 1) / g) + k;
-    return b + k * g;
-}
+// (Tile walks measured and dropped, lab r02h-k: plane chunks slowest, contiguous
+// runs per CTA, smaller blocks of the walk, the order reversed on alternate
+// passes; an L2 prefetch of the G4 block by TMA or LSU, r02e/i.)
 
-// Lab (hint 16384): epilogue warp q pulls the G4 lines of its two blocks of
-// tile t into L2 through the LSU (prefetch.global.L2; the TMA queue stays free
-// for the fills), so the tile's reduces later hit in L2.
-template <class G>
-__device__ __forceinline__ void v3_prefetch_g4(const TmaParams<double>& P, const V3Tile& t, int q, int lane) {
-    constexpr int PP = G::PP, DD = G::DD, PTS = 5;  // 5 points cover a 512-B row segment's lines
-    const int n = P.n;
-#pragma unroll 1
-    for (int i = lane; i < 2 * PP * DD * PTS; i += 32) {
-        const int pt = i % PTS, row = (i / PTS) % DD, pl = (i / (PTS * DD)) % PP, h = i / (PTS * DD * PP);
-        const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
-        const int plane = (int)(t.q0 - P.lo) + PP * wq + pl;
-        const int k1 = t.k1_0 + DD * wr + row;
-        if (plane >= (int)(P.hi - P.lo) || k1 >= n) continue;
-        int k2 = t.j0 + DD * wr + row + (pt == 4 ? 31 : 8 * pt);
-        while (k2 >= n) k2 -= n;
-        const Cx<double>* a = P.g4 + ((int64_t)plane * n + k1) * n + k2;
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(a));
-    }
+// Which tile a CTA takes next.  Static: CTA c takes c, c + grid, ...  Dynamic
+// (P.sched, default): its first tile is c, then each CTA's producer claims the
+// next tile of the L2-aware order from a global counter, so CTAs that run
+// ahead (13.84 tiles each at the bench shape, and uneven L2 luck) take the
+// remainder instead of idling while the slowest finishes.
+__device__ __forceinline__ int v3_next(const TmaParams<double>& P, int k) {
+    if (!P.sched) return (int)blockIdx.x + k * (int)gridDim.x;
+    if (k == 0) return (int)blockIdx.x;
+    return (int)gridDim.x + atomicAdd(P.sched, 1);
 }
-
-// The load/add/store epilogue (hint 131072): instead of adding each parked
-// chunk into the slice with an L2 reduction (RMW inside L2, measured to cap at
-// 5.3 TB/s on its own, tools/rmw_bench.cu), the warp loads the chunk's G4 rows
-// into its park slot by TMA ahead of time (NPARK - 2 chunks ahead, across tile
-// boundaries, so the next tile's first loads overlap the consumers' compute),
-// adds its TMEM values and stores the chunk back by TMA (6.5 TB/s alone).  The
-// sum per entry is the same IEEE add as the L2 reduction's, so results are
-// bitwise those of the reduce path.  Edge chunks (row wrap, last column strip)
-// keep the reduce path.
-template <class G>
-__device__ __forceinline__ void epilogue_ls(const TmaParams<double>& P, int ntiles, int my_tiles, int q, int lane,
-                                            uint32_t tq, uint64_t* tfull, uint64_t* tready, uint64_t* pbar,
-                                            uint32_t park, unsigned char* smem_raw) {
-    constexpr int PP = G::PP, DD = G::DD, NPARK = G::NPARK, LA = NPARK - 2;
-    static_assert(DD == 4, "one 16-column TMEM load per chunk");
-    const int n = P.n;
-    const uint64_t gmap = reinterpret_cast<uint64_t>(&P.gmap);
-    const int drained = (!G::LAST_DIRECT || (P.hints & 1024)) ? my_tiles : my_tiles - 1;
-    // chunk c of a tile: block h = c / np (consumer warp q + 4h), plane p = c % np
-    struct Ck {
-        int plane, k1b, c0, j0e, j0;
-        bool box;
-        uint32_t col;  // TMEM column offset of the chunk in its buffer
-    };
-    auto chunk = [&](const V3Tile& t, int c, int np) {
-        const int h = c / np, p = c % np;
-        const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
-        const int e0 = DD * wr;
-        Ck k;
-        k.plane = (int)(t.q0 - P.lo) + PP * wq + p;
-        k.k1b = t.k1_0 + e0;
-        k.c0 = 2 * (t.j0 - t.k1_0 + n);
-        k.j0e = t.j0 + e0;
-        k.j0 = t.j0;
-        k.box = P.use_gmap && k.k1b + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n;
-        k.col = (uint32_t)(h * G::BLOCK_COLS + p * 16);
-        return k;
-    };
-    auto planes_of = [&](const V3Tile& t) { return min(PP, (int)(P.hi - P.lo) - ((int)(t.q0 - P.lo) + PP * (q % G::CWQ))); };
-    // load cursor: tile lk, chunk lc, sequence lseq
-    int lk = 0, lc = 0, lseq = 0;
-    V3Tile lt = v3_tile<G>(P, v3_lin(P, ntiles, 0));
-    int lnp = drained > 0 ? planes_of(lt) : 0;
-    auto issue_load = [&]() {
-        if (lk >= drained) return;
-        const Ck k = chunk(lt, lc, lnp);
-        const int slot = lseq % NPARK;
-        if (lane == 0) {
-            if (k.box) {
-                mbar_arrive_expect_tx(&pbar[slot], G::CHUNK_BYTES);
-                asm volatile("cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
-                             " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(park + slot * G::CHUNK_BYTES), "l"(gmap),
-                             "r"(k.c0), "r"(k.k1b), "r"(k.plane), "r"(smem_u32(&pbar[slot]))
-                             : "memory");
-            } else {
-                mbar_arrive(&pbar[slot]);  // no load: the phase completes at once
-            }
-        }
-        ++lseq;
-        if (++lc == 2 * lnp) {
-            lc = 0;
-            if (++lk < drained) {
-                lt = v3_tile<G>(P, v3_lin(P, ntiles, lk));
-                lnp = planes_of(lt);
-            }
-        }
-    };
-    for (int i = 0; i < LA; ++i) issue_load();
-    int seq = 0;
-    for (int k = 0; k < drained; ++k) {
-        const int b = k & 1;
-        mbar_wait(&tfull[b], (k >> 1) & 1);
-        tc_fence_after();
-        if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
-        const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
-        const int np = planes_of(t);
-#pragma unroll 1
-        for (int c = 0; c < 2 * np; ++c, ++seq) {
-            const Ck k2 = chunk(t, c, np);
-            const int slot = seq % NPARK;
-            const uint32_t sa = park + slot * G::CHUNK_BYTES + lane * 16;
-            uint32_t v[16];
-            tmem_ld16(tq + b * 256 + k2.col, v);
-            mbar_wait(&pbar[slot], (seq / NPARK) & 1);
-            tmem_wait_ld();
-            if (k2.box) {
-#pragma unroll
-                for (int d = 0; d < DD; ++d) {
-                    double gr, gi;
-                    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(gr), "=d"(gi) : "r"(sa + d * 512) : "memory");
-                    gr = __dadd_rn(gr, __hiloint2double((int)v[4 * d + 1], (int)v[4 * d]));
-                    gi = __dadd_rn(gi, __hiloint2double((int)v[4 * d + 3], (int)v[4 * d + 2]));
-                    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(sa + d * 512), "d"(gr), "d"(gi) : "memory");
-                }
-            } else {
-#pragma unroll
-                for (int d = 0; d < DD; ++d)
-                    asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(sa + d * 512), "r"(v[4 * d]),
-                                 "r"(v[4 * d + 1]), "r"(v[4 * d + 2]), "r"(v[4 * d + 3]) : "memory");
-            }
-            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
-            __syncwarp();
-            if (lane == 0) {
-                const uint32_t sp = park + slot * G::CHUNK_BYTES;
-                if (k2.box)
-                    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];"
-                                 ::"l"(gmap), "r"(sp), "r"(k2.c0), "r"(k2.k1b), "r"(k2.plane) : "memory");
-                else
-                    pst_edge_chunk(P, k2.plane, k2.k1b, k2.j0e, k2.j0, DD,
-                                   reinterpret_cast<const Cx<double>*>(smem_raw + (sp - smem_u32(smem_raw))));
-                asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-                // the slot LA chunks ahead was last used by chunk seq - 2: its store has read it
-                asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
-            }
-            __syncwarp();
-            issue_load();
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 1 + 6 * (q == 3)] = clock64();
-        if (lane == 0) mbar_arrive(&tready[b]);
-    }
-}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
 template <typename RG, class G>
 __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant__ TmaParams<double> P) {
@@ -329,12 +176,12 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     uint64_t* tfull = empty + NST;  // [2] consumers -> epilogue: the tile's blocks are in TMEM buffer b
     uint64_t* tready = tfull + 2;   // [2] epilogue -> consumers: TMEM buffer b has been drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 2);
-    uint64_t* pbar = tready + 3;    // [4][NPARK] G4 chunk loads into the park slots (load/add/store epilogue)
+    int* stage_tile = reinterpret_cast<int*>(tready + 3);  // [NST] tile of a stage's first walker, -1 = end
+    int* buf_tile = stage_tile + NST;                      // [2] tile in TMEM buffer b, -1 = end
 
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = P.nx * ((n + 31) / 32) * ((n + DR - 1) / DR);
-    const int my_tiles = v3_count(P, ntiles);
     const int nb = P.nbatch;
 
     if (threadIdx.x == 0) {
@@ -347,8 +194,11 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             mbar_init(&tfull[b], G::CW);
             mbar_init(&tready[b], 4);
         }
-        for (int i = 0; i < 4 * G::NPARK; ++i) mbar_init(&pbar[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        // the next K1 launch on this stream may start its prologue as our CTAs retire
+        // (programmatic dependent launch; it waits for our completion before it reads
+        // payloads or writes the slice)
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
     if (warp == 8) {  // the whole of TMEM (one CTA per SM)
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
@@ -364,20 +214,28 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         // ---------------- producer ----------------
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_PRODUCER) : "memory");
         if (threadIdx.x == 384) {
+            pdl_wait();  // the payloads may come from the previous kernel on the stream
             const uint64_t keep = l2_policy_evict_last();  // payload rows are re-read by many tiles
             int it = 0;
-            for (int k = 0; k < my_tiles; ++k) {
-                const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
+            int lin = v3_next(P, 0);
+            for (int k = 0;; ++k) {
+                if (lin >= ntiles) {  // end marker: a stage that completes with no bytes
+                    const int s = it % NST;
+                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    stage_tile[s] = -1;
+                    mbar_arrive(&full[s]);
+                    break;
+                }
+                const int nxt = v3_next(P, k + 1);  // claimed a tile ahead: the atomic's latency hides
+                const V3Tile t = v3_tile<G>(P, lin);
                 const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
                 const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
                 const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
                 const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;
-                for (int w = 0; w < nb && !(P.hints & 32); ++w, ++it) {
+                for (int w = 0; w < nb; ++w, ++it) {
                     const int s = it % NST;
-                    if (it >= NST) {
-                        if (P.hints & 64) mbar_wait_sleep(&empty[s], ((it / NST) - 1) & 1);
-                        else mbar_wait(&empty[s], ((it / NST) - 1) & 1);
-                    }
+                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    if (w == 0) stage_tile[s] = lin;  // published by the arrive below (release)
                     mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
                     unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
                     if (P.hints & 2) {
@@ -388,6 +246,11 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                         tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
                     }
                 }
+                lin = nxt;
+            }
+            if (P.sched && atomicAdd(P.sched + 1, 1) == (int)gridDim.x - 1) {
+                P.sched[0] = 0;  // the last producer to finish re-arms the counter slot
+                P.sched[1] = 0;
             }
             trace_gt(P.trace, 4);
         }
@@ -404,22 +267,17 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                                lane * (uint32_t)sizeof(Cx<R>);
         const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
         const uint64_t gmap = reinterpret_cast<uint64_t>(&P.gmap);
-        const uint64_t stream = l2_policy_evict_first();  // slice lines are touched once per pass
-        if (P.hints & 131072) {
-            epilogue_ls<G>(P, ntiles, my_tiles, q, lane, tq, tfull, tready, pbar + q * G::NPARK,
-                           smem_u32(smem_raw + G::PARK_OFF) + (uint32_t)q * G::NPARK * G::CHUNK_BYTES, smem_raw);
-        } else {
         int pair = 0;  // chunk pairs parked by this warp (slot = pair % NSLOT)
         constexpr int NSLOT = G::NPARK / 2;
-        const int drained = (!G::LAST_DIRECT || (P.hints & 1024)) ? my_tiles : my_tiles - 1;  // see consumers
-        for (int k = 0; k < drained && !(P.hints & 256); ++k) {
+        pdl_wait();    // the previous kernel's slice updates land first
+        for (int k = 0;; ++k) {
             const int b = k & 1;
-            if (P.hints & 16384) v3_prefetch_g4<G>(P, v3_tile<G>(P, v3_lin(P, ntiles, k)), q, lane);
-            if (P.hints & 64) mbar_wait_sleep(&tfull[b], (k >> 1) & 1);
-            else mbar_wait(&tfull[b], (k >> 1) & 1);
+            mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
+            const int lin = buf_tile[b];
+            if (lin < 0) break;
             if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
-            const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
+            const V3Tile t = v3_tile<G>(P, lin);
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
@@ -446,15 +304,10 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                                      "r"(v[4 * i]), "r"(v[4 * i + 1]), "r"(v[4 * i + 2]), "r"(v[4 * i + 3]) : "memory");
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic writes -> TMA reads
                     __syncwarp();
-                    if (lane == 0 && !(P.hints & 16)) {  // 16: lab only (no slice traffic)
+                    if (lane == 0) {
                         const uint32_t sp = slot - lane * (uint32_t)sizeof(Cx<R>);
                         for (int c = 0; c < 2 && p + c < np; ++c) {
-                            if (box && (P.hints & 1))  // one sheared box of the slice map: 32 x DD x 1
-                                asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
-                                             ".L2::cache_hint [%0, {%2, %3, %4}], [%1], %5;" ::"l"(gmap),
-                                             "r"(sp + c * G::CHUNK_BYTES), "r"(c0), "r"(k1b), "r"(p_lo + p + c),
-                                             "l"(stream) : "memory");
-                            else if (box)
+                            if (box)  // one sheared box of the slice map: 32 x DD x 1, added in L2
                                 asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
                                              " [%0, {%2, %3, %4}], [%1];" ::"l"(gmap), "r"(sp + c * G::CHUNK_BYTES),
                                              "r"(c0), "r"(k1b), "r"(p_lo + p + c) : "memory");
@@ -472,7 +325,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             __syncwarp();
             if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 1 + 6 * (q == 3)] = clock64();
             if (lane == 0) mbar_arrive(&tready[b]);
-        }
         }
         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
         if (warp == 8 && lane == 0) trace_gt(P.trace, 3);
@@ -493,9 +345,18 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (warp >> 2) * G::BLOCK_COLS;
     int it = 0;
     int pend = -1;  // TMEM buffer whose stores are issued but not yet announced (tfull)
-    const bool defer_st = !(P.hints & 2048);
-    for (int k = 0; k < my_tiles; ++k) {
-        const V3Tile t = v3_tile<G>(P, v3_lin(P, ntiles, k));
+    // hand an end marker to the epilogue through buffer of tile k (after its previous use drained)
+    auto signal_end = [&](int k) {
+        const int b = k & 1;
+        if (k >= 2) mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
+        if (warp == 0 && lane == 0) buf_tile[b] = -1;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tfull[b]);
+    };
+    mbar_wait(&full[0], 0);
+    int lin = stage_tile[0];
+    for (int k = 0; lin >= 0; ++k) {
+        const V3Tile t = v3_tile<G>(P, lin);
         int ps = 0, pd = 0;
         if constexpr (G::ES == 8) {
             const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
@@ -514,7 +375,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
 #pragma unroll 1
         for (int w = 0; w < nb; ++w, ++it) {
             const int s = it % NST;
-            if (!(P.hints & 32)) mbar_wait(&full[s], (it / NST) & 1);  // 32: lab only (no fills at all)
+            if (w > 0) mbar_wait(&full[s], (it / NST) & 1);  // the first walker's stage was waited for its tile id
             if (it == 0 && warp == 0 && lane == 0) trace_gt(P.trace, 1);
             const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
             const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
@@ -539,11 +400,9 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             // release the stage once its values are consumed (see v2: the refill is
             // an async-proxy write, the last ld.shared may still be in flight)
-            if (!(P.hints & 128)) {  // 128: lab only (no stage release; needs 32)
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&empty[s]);
-            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
             if (pend >= 0) {  // the previous tile's TMEM stores, overlapped with this first walker
                 tmem_wait_st();
                 tc_fence_before();
@@ -552,11 +411,10 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 pend = -1;
             }
         }
-        if (P.hints & 256) {  // lab only: no hand-off (the epilogue skips the tile too)
-            if (lane == 0 && acc[0][0].re == 1.2345) P.g4[0] = acc[PP - 1][DD - 1];
-            continue;
-        }
-        if (G::LAST_DIRECT && k == my_tiles - 1 && !(P.hints & 1024)) {
+        // the next tile (or the end marker): its first stage carries the id
+        mbar_wait(&full[it % NST], (it / NST) & 1);
+        const int next = stage_tile[it % NST];
+        if (G::LAST_DIRECT && next < 0) {
             // The last tile: every stage is idle now (all fills consumed), so the
             // eight warps park their blocks there and reduce them into the slice
             // themselves, in parallel -- the kernel does not end on one epilogue
@@ -572,6 +430,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
+                pdl_wait();  // the previous kernel's slice updates land first
                 const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
                 const int k1b = t.k1_0 + e0;
                 const bool box = P.use_gmap && k1b + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n;
@@ -592,15 +451,13 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             __syncwarp();
             if (warp == 0 && lane == 0) trace_gt(P.trace, 2);
+            signal_end(k);
             break;
         }
         // hand the block to the epilogue through TMEM buffer b
         const int b = k & 1;
         const long long tw0 = P.trace ? clock64() : 0;
-        if (k >= 2) {
-            if (P.hints & 64) mbar_wait_sleep(&tready[b], ((k >> 1) - 1) & 1);
-            else mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
-        }
+        if (k >= 2) mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
         if (P.trace && k < 31 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 3] = clock64() - tw0;
         tc_fence_after();
 #pragma unroll
@@ -616,17 +473,37 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             tmem_st32(tq + b * 256 + c * 32, v);
         }
+        if (warp == 0 && lane == 0) buf_tile[b] = lin;
         if (P.trace && k < 31 && lane == 0 && (warp == 0 || warp == 7))
             P.trace[((size_t)blockIdx.x * 32 + k) * 8 + (warp == 0 ? 2 : 5)] = clock64();
         pend = b;  // announced after the next tile's first walker (or below)
-        if (!defer_st || k == my_tiles - 1) {
+        if (next < 0) {
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tfull[b]);
             pend = -1;
+            signal_end(k + 1);
         }
+        lin = next;
     }
+}
+
+// Counter pairs for the dynamic tile claim: 64 slots per device, handed out
+// round robin (a slot is re-armed by the last CTA of the launch that used it;
+// 64 launches in flight at once would be needed to collide).
+static g4_status sched_slot(int dev, int** out) {
+    static std::mutex mu;
+    static int* bufs[64] = {};
+    static unsigned next[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    const int d = dev & 63;
+    if (!bufs[d]) {
+        G4_CUDA(cudaMalloc(&bufs[d], 64 * 2 * sizeof(int)));
+        G4_CUDA(cudaMemset(bufs[d], 0, 64 * 2 * sizeof(int)));
+    }
+    *out = bufs[d] + 2 * (next[d]++ % 64);
+    return G4_OK;
 }
 
 template <typename RG, class G>
@@ -676,8 +553,20 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
             G4_CUDA(cudaMemsetAsync(trace, 0, (size_t)grid * 32 * 8 * sizeof(long long), st));
             tp.trace = trace;
         }
-        kern<<<grid, G::THREADS, G::SMEM, st>>>(tp);
-        G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_pst launch"));
+        static const bool dynamic = env_int("G4RING_V3_SCHED", 1) != 0;  // 0: static tile assignment (A/B)
+        if (dynamic) G4_TRY(sched_slot(dev, &tp.sched));
+        static const bool pdl = env_int("G4RING_PDL", 1) != 0;  // 0: no programmatic dependent launch (A/B)
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(G::THREADS);
+        lc.dynamicSmemBytes = G::SMEM;
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = attr;
+        lc.numAttrs = pdl ? 1 : 0;
+        G4_TRY(check_cuda(cudaLaunchKernelEx(&lc, kern, tp), "k_accumulate_pst launch"));
         if (trace) {
             std::vector<long long> h((size_t)grid * 32 * 8);
             G4_CUDA(cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(long long), cudaMemcpyDeviceToHost, st));

@@ -180,12 +180,9 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
     int32_t nx;   // plane chunks
     int32_t off;  // sheared-coordinate offset (elements), see make_maps
-    int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS, measurement only): 1/2 L2 evict_first/last hints,
-                    // 16 no slice write-back, 32 no payload fills, 64 sleeping waits, 128 no stage release,
-                    // 256 no TMEM hand-off, 1024 last tile via TMEM, 2048 TMEM-store wait not deferred
-                    // (an L2 prefetch of the tile's G4 block, by TMA at the tile's start, measured
-                    // 6-130 % slower, lab r02e: removed)
+    int32_t hints;  // v3 lab knob (G4RING_V3_HINTS): 2 = L2 evict_last on the payload boxes
     long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
+    int* sched;        // v3 dynamic tile claim counter pair (next, done), else null (static tiles)
 };
 
 // Shared -> global bulk copy by the TMA engine: add (.add reduction) or store.

@@ -107,6 +107,7 @@ def test_k1_config_host_query():
     try:
         assert cfg(512, 64)[:8] == [3, 8, 4, 16, 16, 4, 1, 16] and cfg(512, 64)[8] == 1  # v3: persistent, TMEM
         assert cfg(512, 64, _lib.G4_C128_G64)[0] == 3                          # mixed payloads: v3 too
+        assert cfg(4608, 72)[:6] == [3, 8, 4, 16, 16, 3]                        # N = 4608: geometry 43
         assert cfg(512, 64, _lib.G4_C64)[:5] == [2, 8, 4, 16, 8]               # complex64 slices: geometry 12
         assert cfg(512, 64, nbatch=2)[8] == 0                                  # not for B < 4
         assert cfg(512, 8)[:5] == [2, 8, 2, 8, 8] and cfg(512, 8)[8] == 1      # 8-GPU share: geometry 19, deferred
