@@ -82,6 +82,7 @@ def workload_config(args, n_ranks):
     p_local = max(hi - lo for lo, hi in O.partition(planes, S))
     return {"workload": f"{args.config}: {desc}", "n": n, "planes": planes, "planes_per_gpu": p_local,
             "walkers_per_rank_per_step": args.batch, "subring_size": S, "lanes": lanes,
+            "lane_pipelines": "merged per direction" if (lanes == 1 or args.merged_lanes) else "one per lane",
             "parallelism": f"{n_ranks // S} sub-ring(s) of {S}"}
 
 
@@ -715,9 +716,12 @@ def run_ring(args):
     B = args.batch
     # BASELINE config 3 is 8 GPUs as 2 sub-rings of 4 with 2 walker streams (lanes) per GPU
     S, lanes = ring_shape(args, n_ranks)
+    # several lanes: each its own ring pipeline (comm stream, flags, buffers) -- config 3's
+    # "walker streams feeding independent ring pipelines"; --merged-lanes shares one channel
     cfg = E.ExperimentConfig(n_k=n_k, n_w=n_w, world_size=n_ranks, subring_size=S, lanes=lanes,
                              measurements=B, seed=0, value_mode="float", planes=planes, batch=B,
-                             dtype=args.dtype, gather=False, instrument=False, timeout_s=120.0)
+                             dtype=args.dtype, gather=False, instrument=False, timeout_s=120.0,
+                             lane_rings=lanes > 1 and not args.merged_lanes)
     E.validate_config(cfg)
     dev = E.device_for_rank(rank)
     torch.cuda.set_device(dev)
@@ -956,6 +960,8 @@ def main():
                     help="lab runs: headline + parity check only (no e2e, sweeps, other configs)")
     ap.add_argument("--subring-size", type=int, default=0, help="ring size S for N > 1 (default N; c3: 4)")
     ap.add_argument("--lanes", type=int, default=0, help="walker streams per GPU for N > 1 (default 1; c3: 2)")
+    ap.add_argument("--merged-lanes", action="store_true",
+                    help="N > 1: lanes sharing a direction share one ring channel (default: a pipeline per lane)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3

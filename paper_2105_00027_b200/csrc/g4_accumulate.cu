@@ -869,7 +869,7 @@ static int v2_geom(int n, int64_t planes, bool deferred, bool c64_slice, int nba
     // With few walkers per pass the persistent kernel's fixed hand-off and
     // slice reduction per tile dominate: geometry 25 below V3_MIN_WALKERS.
     if (c64_slice) return 12;
-    static const int v3_min = env_int("G4RING_V3_MIN_WALKERS", 6);
+    static const int v3_min = env_int("G4RING_V3_MIN_WALKERS", 8);
     if (nbatch < v3_min) return 25;
     return n > 2048 ? 43 : 40;
 }

@@ -54,8 +54,7 @@ struct V3Geom {
     static constexpr uint32_t PARK_OFF = NST * STAGE_BYTES;
     static constexpr uint32_t PARK_BYTES = 4 * NPARK * CHUNK_BYTES;
     static constexpr uint32_t BAR_OFF = PARK_OFF + PARK_BYTES;
-    // barriers (full/empty per stage, tfull/tready x 2), then the TMEM address and the tile ids
-    static constexpr size_t SMEM = BAR_OFF + (2 * NST + 4) * sizeof(uint64_t) + 8 + (NST + 2) * sizeof(int) + 8;
+    static constexpr size_t SMEM = BAR_OFF + (2 * NST + 4) * sizeof(uint64_t) + 16;
     static constexpr int BLOCK_COLS = PP * DD * 4;          // TMEM columns per consumer warp block
     // the last tile's blocks (CW x PP chunks) fit the idle stage buffers: consumers write it back
     static constexpr bool LAST_DIRECT = (size_t)CW * PP * CHUNK_BYTES <= (size_t)NST * STAGE_BYTES;
@@ -153,19 +152,17 @@ __device__ __forceinline__ V3Tile v3_tile(const TmaParams<double>& P, int lin) {
 // runs per CTA, smaller blocks of the walk, the order reversed on alternate
 // passes; an L2 prefetch of the G4 block by TMA or LSU, r02e/i.)
 
-// Which tile a CTA takes next.  Static: CTA c takes c, c + grid, ...  Dynamic
-// (P.sched, default): its first tile is c, then each CTA's producer claims the
-// next tile of the L2-aware order from a global counter, so CTAs that run
-// ahead (13.84 tiles each at the bench shape, and uneven L2 luck) take the
-// remainder instead of idling while the slowest finishes.
-__device__ __forceinline__ int v3_next(const TmaParams<double>& P, int k) {
-    if (!P.sched) return (int)blockIdx.x + k * (int)gridDim.x;
-    if (k == 0) return (int)blockIdx.x;
-    return (int)gridDim.x + atomicAdd(P.sched, 1);
+// The CTA's tiles: CTA c takes tiles c, c + grid, ... of the L2-aware order.
+// (A dynamic claim from a global counter was measured 20 % slower, lab r02l:
+// it breaks the waves' shared payload rows in L2.)
+__device__ __forceinline__ int v3_count(int ntiles) {
+    const int b = (int)blockIdx.x, g = (int)gridDim.x;
+    return b < ntiles ? (ntiles - 1 - b) / g + 1 : 0;
 }
+__device__ __forceinline__ int v3_lin(int k) { return (int)blockIdx.x + k * (int)gridDim.x; }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-template <typename RG, class G>
+template <typename RG, class G, bool EARLY_ST>
 __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant__ TmaParams<double> P) {
     using R = double;
     constexpr int PP = G::PP, DD = G::DD, NST = G::NST, DR = G::DR;
@@ -176,12 +173,11 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     uint64_t* tfull = empty + NST;  // [2] consumers -> epilogue: the tile's blocks are in TMEM buffer b
     uint64_t* tready = tfull + 2;   // [2] epilogue -> consumers: TMEM buffer b has been drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 2);
-    int* stage_tile = reinterpret_cast<int*>(tready + 3);  // [NST] tile of a stage's first walker, -1 = end
-    int* buf_tile = stage_tile + NST;                      // [2] tile in TMEM buffer b, -1 = end
 
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = P.nx * ((n + 31) / 32) * ((n + DR - 1) / DR);
+    const int my_tiles = v3_count(ntiles);
     const int nb = P.nbatch;
 
     if (threadIdx.x == 0) {
@@ -217,17 +213,8 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             pdl_wait();  // the payloads may come from the previous kernel on the stream
             const uint64_t keep = l2_policy_evict_last();  // payload rows are re-read by many tiles
             int it = 0;
-            int lin = v3_next(P, 0);
-            for (int k = 0;; ++k) {
-                if (lin >= ntiles) {  // end marker: a stage that completes with no bytes
-                    const int s = it % NST;
-                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
-                    stage_tile[s] = -1;
-                    mbar_arrive(&full[s]);
-                    break;
-                }
-                const int nxt = v3_next(P, k + 1);  // claimed a tile ahead: the atomic's latency hides
-                const V3Tile t = v3_tile<G>(P, lin);
+            for (int k = 0; k < my_tiles; ++k) {
+                const V3Tile t = v3_tile<G>(P, v3_lin(k));
                 const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
                 const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
                 const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
@@ -235,7 +222,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 for (int w = 0; w < nb; ++w, ++it) {
                     const int s = it % NST;
                     if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
-                    if (w == 0) stage_tile[s] = lin;  // published by the arrive below (release)
                     mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
                     unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
                     if (P.hints & 2) {
@@ -246,11 +232,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                         tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
                     }
                 }
-                lin = nxt;
-            }
-            if (P.sched && atomicAdd(P.sched + 1, 1) == (int)gridDim.x - 1) {
-                P.sched[0] = 0;  // the last producer to finish re-arms the counter slot
-                P.sched[1] = 0;
             }
             trace_gt(P.trace, 4);
         }
@@ -270,14 +251,13 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         int pair = 0;  // chunk pairs parked by this warp (slot = pair % NSLOT)
         constexpr int NSLOT = G::NPARK / 2;
         pdl_wait();    // the previous kernel's slice updates land first
-        for (int k = 0;; ++k) {
+        const int drained = G::LAST_DIRECT ? my_tiles - 1 : my_tiles;  // see consumers
+        for (int k = 0; k < drained; ++k) {
             const int b = k & 1;
             mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
-            const int lin = buf_tile[b];
-            if (lin < 0) break;
             if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
-            const V3Tile t = v3_tile<G>(P, lin);
+            const V3Tile t = v3_tile<G>(P, v3_lin(k));
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
@@ -345,18 +325,8 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (warp >> 2) * G::BLOCK_COLS;
     int it = 0;
     int pend = -1;  // TMEM buffer whose stores are issued but not yet announced (tfull)
-    // hand an end marker to the epilogue through buffer of tile k (after its previous use drained)
-    auto signal_end = [&](int k) {
-        const int b = k & 1;
-        if (k >= 2) mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
-        if (warp == 0 && lane == 0) buf_tile[b] = -1;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tfull[b]);
-    };
-    mbar_wait(&full[0], 0);
-    int lin = stage_tile[0];
-    for (int k = 0; lin >= 0; ++k) {
-        const V3Tile t = v3_tile<G>(P, lin);
+    for (int k = 0; k < my_tiles; ++k) {
+        const V3Tile t = v3_tile<G>(P, v3_lin(k));
         int ps = 0, pd = 0;
         if constexpr (G::ES == 8) {
             const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
@@ -375,7 +345,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
 #pragma unroll 1
         for (int w = 0; w < nb; ++w, ++it) {
             const int s = it % NST;
-            if (w > 0) mbar_wait(&full[s], (it / NST) & 1);  // the first walker's stage was waited for its tile id
+            mbar_wait(&full[s], (it / NST) & 1);
             if (it == 0 && warp == 0 && lane == 0) trace_gt(P.trace, 1);
             const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
             const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
@@ -385,6 +355,14 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
 #pragma unroll
             for (int d = 0; d < DD; ++d) dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
             constexpr int NJ = PP + DD - 1;  // diagonals p - d
+            // The tile's last walker hands the block to TMEM as it completes: the
+            // 8 entries of store c (planes 2c, 2c+1) are final after diagonal
+            // j = 2c + DD, so each store overlaps the remaining diagonals' math.
+            const bool early = EARLY_ST && w == nb - 1 && !(G::LAST_DIRECT && k == my_tiles - 1);
+            if (early) {
+                if (k >= 2) mbar_wait(&tready[k & 1], ((k >> 1) - 1) & 1);
+                tc_fence_after();
+            }
             Stg<R> S = widen<R>(lds_plain(sh_u + sh_o, sh_d + sh_o));
 #pragma unroll
             for (int j = 0; j < NJ; ++j) {
@@ -397,6 +375,21 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                     update_fused(acc[p][d], S, dv[d]);
                 }
                 if (j + 1 < NJ) S = Sn;
+                if constexpr (PP * DD / 8 == PP / 2 && DD == 4) {
+                    if (early && j >= DD && (j - DD) % 2 == 0 && (j - DD) / 2 < PP / 2) {
+                        const int c = (j - DD) / 2;
+                        uint32_t v[32];
+#pragma unroll
+                        for (int i = 0; i < 8; ++i) {
+                            const Cx<R>& a = acc[(8 * c + i) / DD][(8 * c + i) % DD];
+                            v[4 * i + 0] = (uint32_t)__double2loint(a.re);
+                            v[4 * i + 1] = (uint32_t)__double2hiint(a.re);
+                            v[4 * i + 2] = (uint32_t)__double2loint(a.im);
+                            v[4 * i + 3] = (uint32_t)__double2hiint(a.im);
+                        }
+                        tmem_st32(tq + (k & 1) * 256 + c * 32, v);
+                    }
+                }
             }
             // release the stage once its values are consumed (see v2: the refill is
             // an async-proxy write, the last ld.shared may still be in flight)
@@ -411,10 +404,8 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 pend = -1;
             }
         }
-        // the next tile (or the end marker): its first stage carries the id
-        mbar_wait(&full[it % NST], (it / NST) & 1);
-        const int next = stage_tile[it % NST];
-        if (G::LAST_DIRECT && next < 0) {
+        const bool last = k == my_tiles - 1;
+        if (G::LAST_DIRECT && last) {
             // The last tile: every stage is idle now (all fills consumed), so the
             // eight warps park their blocks there and reduce them into the slice
             // themselves, in parallel -- the kernel does not end on one epilogue
@@ -451,12 +442,12 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             __syncwarp();
             if (warp == 0 && lane == 0) trace_gt(P.trace, 2);
-            signal_end(k);
             break;
         }
         // hand the block to the epilogue through TMEM buffer b
         const int b = k & 1;
         const long long tw0 = P.trace ? clock64() : 0;
+        if (!EARLY_ST) {
         if (k >= 2) mbar_wait(&tready[b], ((k >> 1) - 1) & 1);
         if (P.trace && k < 31 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 3] = clock64() - tw0;
         tc_fence_after();
@@ -473,43 +464,25 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             }
             tmem_st32(tq + b * 256 + c * 32, v);
         }
-        if (warp == 0 && lane == 0) buf_tile[b] = lin;
+        }
         if (P.trace && k < 31 && lane == 0 && (warp == 0 || warp == 7))
             P.trace[((size_t)blockIdx.x * 32 + k) * 8 + (warp == 0 ? 2 : 5)] = clock64();
         pend = b;  // announced after the next tile's first walker (or below)
-        if (next < 0) {
+        if (last) {
             tmem_wait_st();
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&tfull[b]);
             pend = -1;
-            signal_end(k + 1);
         }
-        lin = next;
     }
-}
-
-// Counter pairs for the dynamic tile claim: 64 slots per device, handed out
-// round robin (a slot is re-armed by the last CTA of the launch that used it;
-// 64 launches in flight at once would be needed to collide).
-static g4_status sched_slot(int dev, int** out) {
-    static std::mutex mu;
-    static int* bufs[64] = {};
-    static unsigned next[64] = {};
-    std::lock_guard<std::mutex> lk(mu);
-    const int d = dev & 63;
-    if (!bufs[d]) {
-        G4_CUDA(cudaMalloc(&bufs[d], 64 * 2 * sizeof(int)));
-        G4_CUDA(cudaMemset(bufs[d], 0, 64 * 2 * sizeof(int)));
-    }
-    *out = bufs[d] + 2 * (next[d]++ % 64);
-    return G4_OK;
 }
 
 template <typename RG, class G>
 static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                               int32_t nbatch, cudaStream_t st) {
-    auto kern = k_accumulate_pst<RG, G>;
+    static const bool early = env_int("G4RING_V3_EARLY_ST", 1) != 0;  // 0: stores after the last walker (A/B)
+    auto kern = early ? k_accumulate_pst<RG, G, true> : k_accumulate_pst<RG, G, false>;
     int dev = 0;
     G4_CUDA(cudaGetDevice(&dev));
     {  // the >48 KB shared-memory opt-in is per device
@@ -553,8 +526,6 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
             G4_CUDA(cudaMemsetAsync(trace, 0, (size_t)grid * 32 * 8 * sizeof(long long), st));
             tp.trace = trace;
         }
-        static const bool dynamic = env_int("G4RING_V3_SCHED", 1) != 0;  // 0: static tile assignment (A/B)
-        if (dynamic) G4_TRY(sched_slot(dev, &tp.sched));
         static const bool pdl = env_int("G4RING_PDL", 1) != 0;  // 0: no programmatic dependent launch (A/B)
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(grid);

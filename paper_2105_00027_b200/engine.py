@@ -87,6 +87,9 @@ class ExperimentConfig:
     sample_planes: tuple[int, ...] = ()  # K3 planes copied to world rank 0 (report.samples)
     arith: str = "exact"           # K1 arithmetic: "exact" (bitwise reference order) or "fused" (FMA
                                    # chains + deferred update, within 1e-12; g4_set_arith_mode)
+    lane_rings: bool = False       # every lane its own ring pipeline (comm stream, flags, buffers),
+                                   # as the reference's per-lane rings; False: lanes sharing a
+                                   # direction share one channel (one copy per step)
     # test hooks (never part of a user config, as in the reference)
     ring_steps_override: int | None = None
     fault: str | None = None
@@ -350,7 +353,7 @@ class RingEngine:
         self.code = accumulate_dtype_code(self.dtype, self.pdtype)
         self.pcode = _dtype_code(self.pdtype)
         self.slice = GtSlice.zeros(self.space, self.lo, self.hi, device=device, dtype=self.dtype)
-        self.channels = S.make_channels(self.topo, self.pos)
+        self.channels = S.make_channels(self.topo, self.pos, per_lane=cfg.lane_rings)
         self.lib = _lib.load()
         _lib.check(self.lib.g4_preload_ring_kernels(), "preload_ring_kernels")
         # per channel: 3 buffers (GEN, R0, R1) x batch x lanes staged payloads

@@ -106,13 +106,19 @@ class Channel:
     backward: bool
 
 
-def make_channels(topo: RingTopology, pos: int) -> list[Channel]:
-    groups: dict[tuple[int, int], list[int]] = {}
+def make_channels(topo: RingTopology, pos: int, per_lane: bool = False) -> list[Channel]:
+    """The rank's channels: by default lanes that share a direction (same
+    neighbours) share one channel -- one copy per step carries all their
+    payloads.  per_lane=True gives every lane its own channel (own comm stream,
+    flags and buffers), i.e. the reference's independent per-lane rings
+    (engine.py:62-83) as independent device pipelines."""
+    groups: dict[tuple[int, ...], list[int]] = {}
     for t in range(topo.lanes):
         ring = lane_ring_id(topo, pos, t)
-        groups.setdefault((ring.recv_from, ring.send_to), []).append(t)
+        key = (ring.recv_from, ring.send_to) + ((t,) if per_lane else ())
+        groups.setdefault(key, []).append(t)
     out = []
-    for i, ((rf, st), lanes) in enumerate(sorted(groups.items(), key=lambda kv: kv[1][0])):
+    for i, ((rf, st, *_), lanes) in enumerate(sorted(groups.items(), key=lambda kv: kv[1][0])):
         backward = topo.direction == "alternate" and lanes[0] % 2 == 1
         out.append(Channel(i, tuple(lanes), rf, st, backward))
     return out

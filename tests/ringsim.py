@@ -43,14 +43,14 @@ class RankState:
 
 
 def run_subring(topo, subring, n, lo_hi, seed, rounds, batch, mode="integer", steps=None,
-                fault_rank=None, timeout=10.0):
+                fault_rank=None, timeout=10.0, per_lane=False):
     """Run one sub-ring; returns the RankState list (index = position)."""
     s = topo.subring_size
     ranks = []
     for pos in range(s):
         lo, hi = lo_hi[pos]
         ranks.append(RankState(topo, pos, subring * s + pos, subring, n, lo, hi, batch,
-                               S.make_channels(topo, pos)))
+                               S.make_channels(topo, pos, per_lane)))
     errors = []
     threads = []
     for st in ranks:

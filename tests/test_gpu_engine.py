@@ -161,6 +161,7 @@ def check_counts(c, rep):
     dict(world_size=3, subring_size=3, lanes=3, direction="alternate", n_w=3, measurements=5),
     dict(world_size=4, subring_size=4, lanes=1, value_mode="float", n_k=8, n_w=16, planes=64, measurements=16,
          batch=4),
+    dict(world_size=4, subring_size=2, lanes=2, measurements=8, batch=2, lane_rings=True),  # per-lane pipelines
 ])
 def test_native_round_program_matches_host_loop(kw, monkeypatch):
     """The native round program (one C call per round from round 2 on) against

@@ -109,7 +109,8 @@ def test_config4_share_sampled_planes(oracle, cuda_dev, arith):
     _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if arith == "fused" else _lib.G4_ARITH_EXACT))
     try:
         sp = T.CombinedIndexSpace(36, 128)
-        n, lo, hi, B = sp.size, 144, 216, 4
+        n, lo, hi = sp.size, 144, 216
+        B = 8 if arith == "fused" else 4  # fused: v3 from 8 walkers a pass (geometry 43 at this N)
         assert k1_config(n, hi - lo, B)[0] == (3 if arith == "fused" else 2)
         gs = _walkers(sp, 3, "float", B, dev=cuda_dev)
         sl = T.GtSlice.zeros(sp, lo, hi, device=cuda_dev)

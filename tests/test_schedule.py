@@ -50,12 +50,12 @@ class TestTopology:
 
 
 def run_world(world, s, lanes, rounds, batch, n, seed=1234, mode="integer", direction="forward",
-              planes=None, steps=None, fault_rank=None, timeout=10.0):
+              planes=None, steps=None, fault_rank=None, timeout=10.0, per_lane=False):
     topo = S.RingTopology(world, s, lanes, direction)
     planes = n if planes is None else planes
     ranges = O.partition(planes, s)
-    subs = [ringsim.run_subring(topo, sub, n, ranges, seed, rounds, batch, mode, steps, fault_rank, timeout)
-            for sub in range(world // s)]
+    subs = [ringsim.run_subring(topo, sub, n, ranges, seed, rounds, batch, mode, steps, fault_rank, timeout,
+                                per_lane) for sub in range(world // s)]
     full = np.zeros((planes, n, n), np.complex128)
     for pos, (lo, hi) in enumerate(ranges):  # canonical rank-order reduce (base.py:135-148)
         total = subs[0][pos].g4.copy()
@@ -96,6 +96,32 @@ def test_simulated_ring_equals_oracle(n, world, s, lanes, rounds, batch):
                 assert len(st.origins[t]) == len(set(st.origins[t])) == s * m
                 assert all(o[2] == t and o[0] == st.subring for o in st.origins[t])
             assert st.isolation_violations == 0
+
+
+@pytest.mark.parametrize("world,s,lanes,direction", [(4, 4, 3, "forward"), (4, 2, 2, "forward"),
+                                                     (6, 3, 3, "alternate"), (8, 4, 2, "forward")])
+def test_lane_rings_equal_oracle(world, s, lanes, direction):
+    """Every lane its own ring pipeline (lane_rings): same tensor, same laws."""
+    n, rounds, batch = 8, 2, 2
+    topo, subs, full = run_world(world, s, lanes, rounds, batch, n, direction=direction, per_lane=True)
+    assert all(len(st.channels) == lanes for sub in subs for st in sub)
+    m = rounds * batch
+    assert np.array_equal(full, O.oracle_full(1234, n, world // s, s, lanes, m, "integer"))
+    for sub in subs:
+        for st in sub:
+            for t in range(lanes):
+                assert st.sent[t] == st.received[t] == (s - 1) * m and st.accumulated[t] == s * m
+                assert len(st.origins[t]) == len(set(st.origins[t])) == s * m
+            assert st.isolation_violations == 0
+
+
+def test_lane_rings_template_periodic():
+    topo = S.RingTopology(8, 4, 2, "forward")
+    ch = S.make_channels(topo, 1, per_lane=True)
+    assert [c.lanes for c in ch] == [(0,), (1,)] and [c.index for c in ch] == [0, 1]
+    for par in (0, 1):
+        tpl = S.steady_state_template(topo, 1, ch, par)
+        assert len(tpl) == len(S.round_schedule(topo, 1, ch, 2 + par))
 
 
 @pytest.mark.parametrize("direction", ["forward", "alternate"])
