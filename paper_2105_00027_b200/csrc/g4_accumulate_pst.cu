@@ -481,7 +481,10 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
 template <typename RG, class G>
 static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                               int32_t nbatch, cudaStream_t st) {
-    static const bool early = env_int("G4RING_V3_EARLY_ST", 1) != 0;  // 0: stores after the last walker (A/B)
+    // TMEM stores inside the last walker: -4 % at N = 1024 and -5 % at N = 4608,
+    // +5 % at N = 512 (lab r02n), so from N = 1024 on (G4RING_V3_EARLY_ST=0/1 forces)
+    static const int early_env = env_int("G4RING_V3_EARLY_ST", -1);
+    const bool early = early_env >= 0 ? early_env != 0 : n >= 1024;
     auto kern = early ? k_accumulate_pst<RG, G, true> : k_accumulate_pst<RG, G, false>;
     int dev = 0;
     G4_CUDA(cudaGetDevice(&dev));
@@ -490,7 +493,10 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         static uint64_t done = 0;
         std::lock_guard<std::mutex> lk(mu);
         if (!(done & (1ull << (dev & 63)))) {
-            G4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+            G4_CUDA(cudaFuncSetAttribute(k_accumulate_pst<RG, G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)G::SMEM));
+            G4_CUDA(cudaFuncSetAttribute(k_accumulate_pst<RG, G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)G::SMEM));
             done |= 1ull << (dev & 63);
         }
     }
