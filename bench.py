@@ -720,7 +720,8 @@ def run_ring(args):
     # "walker streams feeding independent ring pipelines"; --merged-lanes shares one channel
     cfg = E.ExperimentConfig(n_k=n_k, n_w=n_w, world_size=n_ranks, subring_size=S, lanes=lanes,
                              measurements=B, seed=0, value_mode="float", planes=planes, batch=B,
-                             dtype=args.dtype, gather=False, instrument=False, timeout_s=120.0,
+                             dtype={"mixed": "c128g64"}.get(args.dtype, args.dtype), gather=False,
+                             instrument=False, timeout_s=120.0,
                              lane_rings=lanes > 1 and not args.merged_lanes)
     E.validate_config(cfg)
     dev = E.device_for_rank(rank)
@@ -728,7 +729,7 @@ def run_ring(args):
     sub = E.build_subrings(world, S)
     eng = E.RingEngine(cfg, sub, rank, dev)
     n = eng.space.size
-    eb = 16 if args.dtype == "c128" else 8
+    eb = 8 if args.dtype == "c64" else 16  # G4 slice entry (mixed: complex128 slice)
     # resident payloads: generate GEN once (K3), untimed
     eng.enqueue_round()
     eng.wait_idle(120.0)
