@@ -798,9 +798,9 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 40:
         case 42:
         case 43:
-        case 44:  // v3, the persistent kernel: fused + deferred, complex128 slices only
-            if constexpr (FUSED && sizeof(R) == 8)
-                return launch_pst<RG>(g, prm.g4, prm.lo, prm.hi, prm.n,
+        case 44:  // v3, the persistent kernel (complex128 slices): fused + deferred, or exact
+            if constexpr (sizeof(R) == 8)
+                return launch_pst<RG>(g, !FUSED, prm.g4, prm.lo, prm.hi, prm.n,
                                       reinterpret_cast<const void* const*>(prm.stg), prm.nbatch, st);
             return launch_v2_geom<R, RG, FUSED>(FUSED ? 12 : 13, prm, st);
         default: return fail(G4_ERR_CONTRACT, "G4RING_V2GEOM: unknown geometry");
@@ -860,7 +860,11 @@ static int v2_geom(int n, int64_t planes, bool deferred, bool c64_slice, int nba
     }
     if (forced >= 0) return forced;
     if (planes < 16) return 19;
-    if (!deferred) return 13;
+    if (!deferred) {  // exact mode (bitwise): geometry 13, or v3's exact variant (G4RING_V3_EXACT=1, lab)
+        static const int v3_exact = env_int("G4RING_V3_EXACT", 0);
+        if (v3_exact && !c64_slice && nbatch >= 8) return n > 2048 ? 43 : 40;
+        return 13;
+    }
     // complex128 slices: the persistent TMEM-handoff kernel (v3).  Geometry 40
     // (4 stages, 4 park slots) at N <= 1024; at N = 4608 the slice reduces miss
     // L2 far more and geometry 43 (3 stages, 10 park slots) wins, 13.9 ms vs

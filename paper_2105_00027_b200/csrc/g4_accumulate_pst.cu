@@ -106,6 +106,7 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 // rows past N skipped, columns split at the row end.  Edge tiles only (one lane).
 // Inlined: an ABI call from a setmaxnreg-reduced warp group may use registers the
 // group no longer owns (a __noinline__ version corrupted the edge chunks).
+template <bool ADD = true>
 __device__ __forceinline__ void pst_edge_chunk(const TmaParams<double>& P, int plane, int k1b, int k2b, int j0, int dd,
                                             const Cx<double>* park) {
     const int n = P.n;
@@ -118,8 +119,8 @@ __device__ __forceinline__ void pst_edge_chunk(const TmaParams<double>& P, int p
         if (k2 >= n) k2 -= n;
         Cx<double>* row = base + (int64_t)k1 * n;
         const int run1 = min(cnt, n - k2);
-        segment_out<true, double>(row + k2, park + d * 32, run1);
-        if (run1 < cnt) segment_out<true, double>(row, park + d * 32 + run1, cnt - run1);
+        segment_out<ADD, double>(row + k2, park + d * 32, run1);
+        if (run1 < cnt) segment_out<ADD, double>(row, park + d * 32 + run1, cnt - run1);
     }
 }
 // Lab timeline (G4RING_V3_TRACE): row 31 of a CTA's trace holds %globaltimer
@@ -162,7 +163,38 @@ __device__ __forceinline__ int v3_count(int ntiles) {
 __device__ __forceinline__ int v3_lin(int k) { return (int)blockIdx.x + k * (int)gridDim.x; }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
-template <typename RG, class G, bool EARLY_ST>
+// G4_ARITH_EXACT in the same structure: the reference op order per walker
+// (u*down + d*up rounded, then added), the consumers load their block at the
+// tile's start (the epilogue has pulled it into L2 while the previous tile
+// computed) and the epilogue stores instead of reducing.
+template <typename R>
+__device__ __forceinline__ void update_exact(Cx<R>& a, const Stg<R>& S, const Stg<R>& D) {
+    R p1r, p1i, p2r, p2i;
+    cmul(S.ur, S.ui, D.dr, D.di, p1r, p1i);  // u * down[k2][k1]
+    cmul(S.dr, S.di, D.ur, D.ui, p2r, p2i);  // d * up[k2][k1]
+    a.re = add_rn(a.re, add_rn(p1r, p2r));
+    a.im = add_rn(a.im, add_rn(p1i, p2i));
+}
+// Exact mode: epilogue warp q pulls the G4 rows of its two blocks of tile t
+// into L2 (prefetch.global.L2, 5 points per 512-B row segment).
+template <class G>
+__device__ __forceinline__ void v3_prefetch_g4(const TmaParams<double>& P, const V3Tile& t, int q, int lane) {
+    constexpr int PP = G::PP, DD = G::DD, PTS = 5;
+    const int n = P.n;
+#pragma unroll 1
+    for (int i = lane; i < 2 * PP * DD * PTS; i += 32) {
+        const int pt = i % PTS, row = (i / PTS) % DD, pl = (i / (PTS * DD)) % PP, h = i / (PTS * DD * PP);
+        const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
+        const int plane = (int)(t.q0 - P.lo) + PP * wq + pl;
+        const int k1 = t.k1_0 + DD * wr + row;
+        if (plane >= (int)(P.hi - P.lo) || k1 >= n) continue;
+        int k2 = t.j0 + DD * wr + row + (pt == 4 ? 31 : 8 * pt);
+        while (k2 >= n) k2 -= n;
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(P.g4 + ((int64_t)plane * n + k1) * n + k2));
+    }
+}
+
+template <typename RG, class G, bool EARLY_ST, bool EXACT>
 __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant__ TmaParams<double> P) {
     using R = double;
     constexpr int PP = G::PP, DD = G::DD, NST = G::NST, DR = G::DR;
@@ -254,6 +286,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         const int drained = G::LAST_DIRECT ? my_tiles - 1 : my_tiles;  // see consumers
         for (int k = 0; k < drained; ++k) {
             const int b = k & 1;
+            if (EXACT && k + 1 < my_tiles) v3_prefetch_g4<G>(P, v3_tile<G>(P, v3_lin(k + 1)), q, lane);
             mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
             if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
@@ -287,12 +320,16 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                     if (lane == 0) {
                         const uint32_t sp = slot - lane * (uint32_t)sizeof(Cx<R>);
                         for (int c = 0; c < 2 && p + c < np; ++c) {
-                            if (box)  // one sheared box of the slice map: 32 x DD x 1, added in L2
+                            if (box && EXACT)  // one sheared box of the slice map: 32 x DD x 1, stored
+                                asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group"
+                                             " [%0, {%2, %3, %4}], [%1];" ::"l"(gmap), "r"(sp + c * G::CHUNK_BYTES),
+                                             "r"(c0), "r"(k1b), "r"(p_lo + p + c) : "memory");
+                            else if (box)  // ... added in L2
                                 asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
                                              " [%0, {%2, %3, %4}], [%1];" ::"l"(gmap), "r"(sp + c * G::CHUNK_BYTES),
                                              "r"(c0), "r"(k1b), "r"(p_lo + p + c) : "memory");
                             else
-                                pst_edge_chunk(P, p_lo + p + c, k1b, t.j0 + e0, t.j0, DD,
+                                pst_edge_chunk<!EXACT>(P, p_lo + p + c, k1b, t.j0 + e0, t.j0, DD,
                                                reinterpret_cast<const Cx<double>*>(smem_raw + (sp + c * G::CHUNK_BYTES -
                                                                                                smem_u32(smem_raw))));
                         }
@@ -338,10 +375,29 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         const int dr_o = e0 * G::W + lane + pd;                                // direct row d: + d * W
         if (P.trace && k < 31 && lane == 0 && warp == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 4] = clock64();
         Cx<R> acc[PP][DD];
+        if constexpr (EXACT) {  // the block's current values (every entry owned by this tile)
+            if (k == 0) pdl_wait();  // the previous kernel's slice updates land first
+            const int64_t nn = (int64_t)n * n;
+            const int c = t.j0 + lane;
+            const int qw = (int)(t.q0 - P.lo) + PP * wq;
+            const Cx<R>* gb = P.g4 + (int64_t)qw * nn;
 #pragma unroll
-        for (int p = 0; p < PP; ++p)
+            for (int p = 0; p < PP; ++p)
 #pragma unroll
-            for (int d = 0; d < DD; ++d) acc[p][d].re = acc[p][d].im = R(0);
+                for (int d = 0; d < DD; ++d) {
+                    const int k1 = t.k1_0 + e0 + d;
+                    if (c < n && qw + p < (int)(P.hi - P.lo) && k1 < n) {
+                        acc[p][d] = ld_g4(gb + p * nn + (int64_t)k1 * n + wrap(c + e0 + d, n));
+                    } else {
+                        acc[p][d].re = acc[p][d].im = R(0);
+                    }
+                }
+        } else {
+#pragma unroll
+            for (int p = 0; p < PP; ++p)
+#pragma unroll
+                for (int d = 0; d < DD; ++d) acc[p][d].re = acc[p][d].im = R(0);
+        }
 #pragma unroll 1
         for (int w = 0; w < nb; ++w, ++it) {
             const int s = it % NST;
@@ -372,7 +428,8 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 for (int d = 0; d < DD; ++d) {
                     const int p = j + d - (DD - 1);
                     if (p < 0 || p >= PP) continue;
-                    update_fused(acc[p][d], S, dv[d]);
+                    if constexpr (EXACT) update_exact(acc[p][d], S, dv[d]);
+                    else update_fused(acc[p][d], S, dv[d]);
                 }
                 if (j + 1 < NJ) S = Sn;
                 if constexpr (PP * DD / 8 == PP / 2 && DD == 4) {
@@ -427,13 +484,18 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 const bool box = P.use_gmap && k1b + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n;
                 const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
                 for (int p = 0; p < np; ++p) {
-                    if (box)
+                    if (box && EXACT)
+                        asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group"
+                                     " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&P.gmap)),
+                                     "r"(park + p * G::CHUNK_BYTES), "r"(2 * (t.j0 - t.k1_0 + n)), "r"(k1b),
+                                     "r"(p_lo + p) : "memory");
+                    else if (box)
                         asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
                                      " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&P.gmap)),
                                      "r"(park + p * G::CHUNK_BYTES), "r"(2 * (t.j0 - t.k1_0 + n)), "r"(k1b),
                                      "r"(p_lo + p) : "memory");
                     else
-                        pst_edge_chunk(P, p_lo + p, k1b, t.j0 + e0, t.j0, DD,
+                        pst_edge_chunk<!EXACT>(P, p_lo + p, k1b, t.j0 + e0, t.j0, DD,
                                        reinterpret_cast<const Cx<double>*>(smem_raw + (park + p * G::CHUNK_BYTES -
                                                                                        smem_u32(smem_raw))));
                 }
@@ -478,14 +540,14 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     }
 }
 
-template <typename RG, class G>
+template <typename RG, class G, bool EXACT>
 static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                               int32_t nbatch, cudaStream_t st) {
     // TMEM stores inside the last walker: -4 % at N = 1024 and -5 % at N = 4608,
     // +5 % at N = 512 (lab r02n), so from N = 1024 on (G4RING_V3_EARLY_ST=0/1 forces)
     static const int early_env = env_int("G4RING_V3_EARLY_ST", -1);
     const bool early = early_env >= 0 ? early_env != 0 : n >= 1024;
-    auto kern = early ? k_accumulate_pst<RG, G, true> : k_accumulate_pst<RG, G, false>;
+    auto kern = early ? k_accumulate_pst<RG, G, true, EXACT> : k_accumulate_pst<RG, G, false, EXACT>;
     int dev = 0;
     G4_CUDA(cudaGetDevice(&dev));
     {  // the >48 KB shared-memory opt-in is per device
@@ -493,10 +555,10 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         static uint64_t done = 0;
         std::lock_guard<std::mutex> lk(mu);
         if (!(done & (1ull << (dev & 63)))) {
-            G4_CUDA(cudaFuncSetAttribute(k_accumulate_pst<RG, G, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)G::SMEM));
-            G4_CUDA(cudaFuncSetAttribute(k_accumulate_pst<RG, G, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)G::SMEM));
+            G4_CUDA(cudaFuncSetAttribute(k_accumulate_pst<RG, G, true, EXACT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
+            G4_CUDA(cudaFuncSetAttribute(k_accumulate_pst<RG, G, false, EXACT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
             done |= 1ull << (dev & 63);
         }
     }
@@ -562,20 +624,26 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
 //   40: 8x4 blocks, 2x4 warps (tile 16 planes x 16 diagonals), 4 stages, 4 park slots
 //   (a 32 x 8 tile, 4x2 warps, needs a band of 39 rows + 32 columns: beyond the staged halo)
 //   42: as 40 with 3 stages and 8 park slots; 43: 3 stages, 10 park slots; 44: 2 stages, 16 park slots
+template <typename RG, class G>
+static g4_status launch_pst_mode(bool exact, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                                 int32_t nbatch, cudaStream_t st) {
+    return exact ? launch_pst_t<RG, G, true>(g4p, lo, hi, n, staged, nbatch, st)
+                 : launch_pst_t<RG, G, false>(g4p, lo, hi, n, staged, nbatch, st);
+}
 template <typename RG>
-g4_status launch_pst(int geom, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+g4_status launch_pst(int geom, bool exact, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                      int32_t nbatch, cudaStream_t st) {
     switch (geom) {
-        case 40: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 4, 4>>(g4p, lo, hi, n, staged, nbatch, st);
-        case 42: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 3, 8>>(g4p, lo, hi, n, staged, nbatch, st);
-        case 43: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 3, 10>>(g4p, lo, hi, n, staged, nbatch, st);
-        case 44: return launch_pst_t<RG, V3Geom<RG, 8, 4, 2, 4, 2, 16>>(g4p, lo, hi, n, staged, nbatch, st);
+        case 40: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 4, 4>>(exact, g4p, lo, hi, n, staged, nbatch, st);
+        case 42: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 3, 8>>(exact, g4p, lo, hi, n, staged, nbatch, st);
+        case 43: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 3, 10>>(exact, g4p, lo, hi, n, staged, nbatch, st);
+        case 44: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 2, 16>>(exact, g4p, lo, hi, n, staged, nbatch, st);
         default: return fail(G4_ERR_CONTRACT, "unknown v3 geometry");
     }
 }
-template g4_status launch_pst<double>(int, void*, int64_t, int64_t, int32_t, const void* const*, int32_t,
+template g4_status launch_pst<double>(int, bool, void*, int64_t, int64_t, int32_t, const void* const*, int32_t,
                                       cudaStream_t);
-template g4_status launch_pst<float>(int, void*, int64_t, int64_t, int32_t, const void* const*, int32_t,
+template g4_status launch_pst<float>(int, bool, void*, int64_t, int64_t, int32_t, const void* const*, int32_t,
                                      cudaStream_t);
 
 bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst) {

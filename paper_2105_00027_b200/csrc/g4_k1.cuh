@@ -275,7 +275,7 @@ g4_status slice_map(const void* g4, int n, int64_t planes, int pp, int dd, CUten
 // K1 v3 (g4_accumulate_pst.cu): the persistent fused update of a complex128
 // slice with payload entries RG; geometry ids 40-42.
 template <typename RG>
-g4_status launch_pst(int geom, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+g4_status launch_pst(int geom, bool exact, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                      int32_t nbatch, cudaStream_t st);
 bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst);
 
