@@ -64,7 +64,7 @@ def main():
     skew = np.where(ok, tr[:, :, 5] - tr[:, :, 2], 0)[ok]
     wait = tr[:, :, 3][ok]
     total = (np.max(np.where(ok, tr[:, :, 2], 0), 1) - tr[:, 0, 4])
-    pct = lambda x: f"median {np.median(x):8.0f}  p90 {np.percentile(x, 90):8.0f}  max {np.max(x):8.0f}"
+    pct = lambda x: f"median {np.median(x):8.0f}  p90 {np.percentile(x, 90):8.0f}  max {np.max(x):8.0f}  mean {np.mean(x):8.0f}"
     print(f"grid {grid}, tiles per CTA {ntile.min()}-{ntile.max()}, CTA span (cycles): {pct(total)}")
     print(f"consumer tile (w0 start -> w0 done): {pct(dur)}")
     print(f"w7 done - w0 done (warp skew):       {pct(skew)}")
