@@ -364,6 +364,10 @@ def run_gpu(args):
             "sample": f"{max(2, args.cpu_steps)} steps of {B} walkers x {planes} planes x N^2={n * n}, "
                       f"numpy port of accumulate_g4 in {used} processes on disjoint K3 ranges; "
                       f"host {cpu_model()}"}
+        # also one core (8 planes of the same shape; the rate is per update)
+        rate1, _, _ = cpu_throughput(n, min(8, planes), B, 2, 1, 1)
+        line["cpu_baseline"]["one_core"] = {"value": rate1, "unit": "updates/s", "cores": 1,
+                                            "sample": f"2 steps of {B} walkers x {min(8, planes)} planes"}
     print(json.dumps(line), flush=True)
 
 

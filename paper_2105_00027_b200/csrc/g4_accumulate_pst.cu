@@ -194,6 +194,28 @@ __device__ __forceinline__ void v3_prefetch_g4(const TmaParams<double>& P, const
     }
 }
 
+// One slice entry of an edge chunk (row k1, column k2 before the wrap, the lane's
+// column c of the 32-wide strip), by the lane holding it: red.global.add.f64
+// pairs (exact mode: a store).  Rows past N and columns past a partial last
+// strip do not exist.  Each lane writes its own entries, so the warp's row
+// segments stay coalesced -- one lane walking the chunk with bulk ops (the
+// round-2 first cut) took 5.8x an interior drain on the 1/16 of tiles whose
+// row segments wrap (lab r02p/q).
+template <bool EXACT>
+__device__ __forceinline__ void edge_entry(const TmaParams<double>& P, int plane, int k1, int k2, int c, double re,
+                                           double im) {
+    const int n = P.n;
+    if (k1 >= n || c >= n) return;
+    if (k2 >= n) k2 -= n;
+    double* g = reinterpret_cast<double*>(P.g4 + ((int64_t)plane * n + k1) * n + k2);
+    if constexpr (EXACT) {
+        asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(g), "d"(re), "d"(im) : "memory");
+    } else {
+        asm volatile("red.global.add.f64 [%0], %1;" ::"l"(g), "d"(re) : "memory");
+        asm volatile("red.global.add.f64 [%0], %1;" ::"l"(g + 1), "d"(im) : "memory");
+    }
+}
+
 template <typename RG, class G, bool EARLY_ST, bool EXACT>
 __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant__ TmaParams<double> P) {
     using R = double;
@@ -306,6 +328,17 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                     uint32_t v[32];
                     tmem_ld32(tb + p * 16, v);
                     tmem_wait_ld();
+                    if (!box) {  // row wrap / last column strip: every lane adds its own entries
+                        for (int c = 0; c < 2 && p + c < np; ++c)
+#pragma unroll
+                            for (int d = 0; d < DD; ++d) {
+                                const uint32_t* e = v + 4 * (c * DD + d);
+                                edge_entry<EXACT>(P, p_lo + p + c, k1b + d, t.j0 + e0 + d + lane, t.j0 + lane,
+                                                  __hiloint2double((int)e[1], (int)e[0]),
+                                                  __hiloint2double((int)e[3], (int)e[2]));
+                            }
+                        continue;  // no park slot, no bulk group
+                    }
                     const uint32_t slot = park0 + (uint32_t)(pair % NSLOT) * 2 * G::CHUNK_BYTES;
                     if (pair >= NSLOT) {  // the slot's previous reduces have read it
                         if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NSLOT - 1) : "memory");
@@ -320,18 +353,14 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                     if (lane == 0) {
                         const uint32_t sp = slot - lane * (uint32_t)sizeof(Cx<R>);
                         for (int c = 0; c < 2 && p + c < np; ++c) {
-                            if (box && EXACT)  // one sheared box of the slice map: 32 x DD x 1, stored
+                            if (EXACT)  // one sheared box of the slice map: 32 x DD x 1, stored
                                 asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group"
                                              " [%0, {%2, %3, %4}], [%1];" ::"l"(gmap), "r"(sp + c * G::CHUNK_BYTES),
                                              "r"(c0), "r"(k1b), "r"(p_lo + p + c) : "memory");
-                            else if (box)  // ... added in L2
+                            else  // ... added in L2
                                 asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
                                              " [%0, {%2, %3, %4}], [%1];" ::"l"(gmap), "r"(sp + c * G::CHUNK_BYTES),
                                              "r"(c0), "r"(k1b), "r"(p_lo + p + c) : "memory");
-                            else
-                                pst_edge_chunk<!EXACT>(P, p_lo + p + c, k1b, t.j0 + e0, t.j0, DD,
-                                               reinterpret_cast<const Cx<double>*>(smem_raw + (sp + c * G::CHUNK_BYTES -
-                                                                                               smem_u32(smem_raw))));
                         }
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
@@ -468,6 +497,22 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             // themselves, in parallel -- the kernel does not end on one epilogue
             // warp's serial drain of a whole tile.
             asm volatile("barrier.sync 2, %0;" ::"n"(32 * G::CW) : "memory");  // all stage reads done
+            const int p_lo_d = (int)(t.q0 - P.lo) + PP * wq;
+            const int k1b_d = t.k1_0 + e0;
+            if (!(P.use_gmap && k1b_d + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n)) {
+                // an edge block (row wrap / last column strip): every lane adds its own entries
+                pdl_wait();
+                const int np = min(PP, (int)(P.hi - P.lo) - p_lo_d);
+#pragma unroll
+                for (int p = 0; p < PP; ++p)
+#pragma unroll
+                    for (int d = 0; d < DD; ++d)
+                        if (p < np)
+                            edge_entry<EXACT>(P, p_lo_d + p, k1b_d + d, t.j0 + e0 + d + lane, t.j0 + lane,
+                                              acc[p][d].re, acc[p][d].im);
+                if (warp == 0 && lane == 0) trace_gt(P.trace, 2);
+                break;
+            }
             const uint32_t park = smem_u32(smem_raw) + (uint32_t)warp * PP * G::CHUNK_BYTES;
 #pragma unroll
             for (int p = 0; p < PP; ++p)
@@ -586,7 +631,8 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         tp.nx = (int32_t)((hi - lo + G::Q - 1) / G::Q);
         const int64_t tiles = (int64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
         if (tiles >= (1ll << 31)) return fail(G4_ERR_CONTRACT, "accumulate: tile count too large");
-        const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+        static const int grid_env = env_int("G4RING_V3_GRID", 0);  // lab: fewer CTAs than SMs
+        const unsigned grid = (unsigned)std::min<int64_t>(tiles, grid_env > 0 ? std::min(grid_env, sms) : sms);
         static const char* trace_path = getenv("G4RING_V3_TRACE");  // lab: per-tile timeline dump
         long long* trace = nullptr;
         if (trace_path) {

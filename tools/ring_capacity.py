@@ -7,6 +7,9 @@ last plane of every rank's slice are checked against the C oracle.
 
     python tools/ring_capacity.py [--ranks 6] [--measurements 1]
 
+On an 8-GPU node, --ranks 8 is BASELINE config 4 itself: 576 planes, 196 GB of
+G4 across the 8 GPUs, one rank per GPU.
+
 Prints one JSON line (total G4 bytes, per-rank bytes, round time, max
 relative error of the sampled planes).  Measurement tool, not a test.
 """
@@ -22,6 +25,7 @@ ROOT = Path(__file__).resolve().parent.parent
 sys.path.insert(0, str(ROOT))
 
 import numpy as np  # noqa: E402
+import torch  # noqa: E402
 
 from oracle import oracle as O  # noqa: E402
 from paper_2105_00027_b200 import engine as E  # noqa: E402
@@ -55,7 +59,12 @@ def main() -> None:
                       "sampled_planes": list(samples), "max_rel_err": worst, "tolerance": 1e-10,
                       "ok": worst < 1e-10, "wall_s": wall,
                       "round_gpu_ms": {str(r): v for r, v in rep.round_ms.items()},
-                      "note": "all ranks share the box's GPU(s); times are not per-GPU throughput"}),
+                      "per_rank": [{"rank": r, "slice": list(rep.slices[r]), "peak_device_bytes": rep.memory_peaks[r],
+                                    "gpu_ms": rep.round_ms.get(r)} for r in sorted(rep.slices)],
+                      "visible_gpus": torch.cuda.device_count(),
+                      "config4": planes == 576,
+                      "note": ("one rank per GPU" if torch.cuda.device_count() >= a.ranks else
+                               "ranks share the box's GPU(s); times are not per-GPU throughput")}),
           flush=True)
 
 

@@ -72,6 +72,31 @@ def main():
     print(f"epilogue drain q0 (tfull -> tready):  {pct(drain)}")
     print(f"epilogue drain q3:                    {pct(drain3)}")
     print(f"consumer w0 tready wait:             {pct(wait)}  (nonzero in {np.mean(wait > 200) * 100:.0f}% of tiles)")
+    # drains of tiles in the last 32-column strip (their chunks wrap: the edge path) vs the rest
+    n = 512
+    nx, ny, nz = -(-a.planes // 16), -(-n // 32), -(-n // 16)
+
+    def tile_y(lin):  # tile_coord (g4_k1.cuh) with TILE_BY = 16, TILE_BZ = 32: the column chunk
+        per_row = nx * ny * 32
+        br = lin // per_row
+        r = lin - br * per_row
+        bze = min(32, nz - br * 32)
+        per_blk = nx * 16 * bze
+        by = r // per_blk
+        r -= by * per_blk
+        bye = min(16, ny - by * 16)
+        r //= nx
+        return by * 16 + r % bye
+    edge, inner = [], []
+    for c in range(grid):
+        for k in range(min(ntile[c], 31)):
+            d = tr[c, k, 1] - tr[c, k, 0]
+            if tr[c, k, 0] == 0 or tr[c, k, 1] == 0:
+                continue
+            (edge if tile_y(c + k * grid) == ny - 1 else inner).append(d)
+    if edge and inner:
+        print(f"drain q0, edge-strip tiles ({len(edge)}): {pct(np.array(edge))}")
+        print(f"drain q0, interior tiles ({len(inner)}):   {pct(np.array(inner))}")
     g = raw.reshape(a.passes, grid, 32, 8)[-1][:, 31, :5].astype(np.float64)  # globaltimer ns
     t0 = g[:, 0].min()
     us = lambda x: f"median {np.median(x):7.2f}  min {np.min(x):7.2f}  max {np.max(x):7.2f} us"
