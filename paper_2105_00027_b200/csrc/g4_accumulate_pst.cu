@@ -308,7 +308,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         const int drained = G::LAST_DIRECT ? my_tiles - 1 : my_tiles;  // see consumers
         for (int k = 0; k < drained; ++k) {
             const int b = k & 1;
-            if (EXACT && k + 1 < my_tiles) v3_prefetch_g4<G>(P, v3_tile<G>(P, v3_lin(k + 1)), q, lane);
+            if (EXACT && k + 1 < drained) v3_prefetch_g4<G>(P, v3_tile<G>(P, v3_lin(k + 1)), q, lane);
             mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
             if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();

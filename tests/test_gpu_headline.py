@@ -242,7 +242,7 @@ def test_reference_layout_entry_rejects_small_workspace(cuda_dev):
     assert type(e.value).__name__ == "ContractViolation"
 
 
-@pytest.mark.parametrize("geom", ["40", "25", "27", "12", "13", "19"])
+@pytest.mark.parametrize("geom", ["40", "43", "25", "27", "12", "13", "19"])
 def test_forced_geometry_parity_repeated(geom):
     """Each production (and selectable warp-specialised) geometry forced on the
     small-slice suite AND the full N = 512 x 64 x 8 bench shape, exact and

@@ -380,7 +380,11 @@ def test_core_copy_plus_halo_rebuild_is_exact(cuda_dev, n, dtype):
 
 
 @pytest.mark.parametrize("dtype,n,lo,hi,nb", [("c128", 96, 0, 40, 6), ("c64", 96, 3, 37, 5), ("mixed", 128, 0, 24, 8),
-                                              ("c128", 128, 10, 18, 4), ("c128", 160, 0, 20, 3)])
+                                              ("c128", 128, 10, 18, 4), ("c128", 160, 0, 20, 3),
+                                              # K1 v3 (>= 8 walkers, >= 16 planes) with a partial last column
+                                              # strip and row wraps (the per-lane edge path), nonzero start
+                                              ("c128", 200, 5, 45, 8), ("mixed", 150, 0, 33, 12),
+                                              ("c128", 64, 0, 64, 9)])
 def test_fused_deferred_update(oracle, cuda_dev, dtype, n, lo, hi, nb):
     """G4_ARITH_FUSED with >= 4 walkers adds the walkers' sum to a NONZERO slice
     at the end (L2 reduction): integer payloads stay bitwise, float within
