@@ -264,6 +264,24 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         // ---------------- producer ----------------
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_PRODUCER) : "memory");
         if (threadIdx.x == 384) {
+            if (my_tiles > 0) {
+                // Before waiting for the previous kernel: pull this CTA's first
+                // walkers' boxes into L2 (an L2 prefetch reads through the point of
+                // coherence, so it cannot yield stale data for the loads below)
+                const V3Tile t = v3_tile<G>(P, v3_lin(0));
+                const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
+                const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
+                const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
+                const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;
+                for (int w = 0; w < min(nb, NST); ++w) {
+                    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                                 ::"l"(reinterpret_cast<uint64_t>(&P.dmap[w])), "r"(EW * (xd - pd)), "r"(t.k1_0),
+                                 "r"(0) : "memory");
+                    asm volatile("cp.async.bulk.prefetch.tensor.3d.L2.global.tile [%0, {%1, %2, %3}];"
+                                 ::"l"(reinterpret_cast<uint64_t>(&P.smap[w])), "r"(EW * (xs - ps)), "r"(R0),
+                                 "r"(0) : "memory");
+                }
+            }
             pdl_wait();  // the payloads may come from the previous kernel on the stream
             const uint64_t keep = l2_policy_evict_last();  // payload rows are re-read by many tiles
             int it = 0;

@@ -87,6 +87,9 @@ class ExperimentConfig:
     sample_planes: tuple[int, ...] = ()  # K3 planes copied to world rank 0 (report.samples)
     arith: str = "exact"           # K1 arithmetic: "exact" (bitwise reference order) or "fused" (FMA
                                    # chains + deferred update, within 1e-12; g4_set_arith_mode)
+    reduce: str = "peer"           # cross-sub-ring reduce: "peer" (one kernel reading the peers' slices
+                                   # over NVLink, canonical rank order, bitwise = reference) or "nccl"
+                                   # (ncclReduce of the slices viewed as float64; needs one GPU per rank)
     lane_rings: bool = False       # every lane its own ring pipeline (comm stream, flags, buffers),
                                    # as the reference's per-lane rings; False: lanes sharing a
                                    # direction share one channel (one copy per step)
@@ -160,6 +163,8 @@ def validate_config(cfg) -> None:
         raise ConfigError(f"dtype must be c128, c64 or c128g64, got {cfg.dtype!r}")
     if cfg.timeout_s <= 0:
         raise ConfigError("timeout_s must be positive")
+    if cfg.reduce not in ("peer", "nccl"):
+        raise ConfigError(f"reduce must be peer or nccl, got {cfg.reduce!r}")
     if cfg.arith not in ARITH_MODES:
         raise ConfigError(f"arith must be one of {tuple(ARITH_MODES)}, got {cfg.arith!r}")
 
@@ -272,6 +277,31 @@ def reduce_sum(ctl: Control, data: torch.Tensor, root: int = 0) -> None:
         finally:
             pm.close()
     ctl.barrier()
+
+
+def reduce_sum_nccl(world: Control, s: int, data: torch.Tensor) -> None:
+    """The cross-sub-ring reduce as an NCCL collective (north_star item 4): the
+    position group of this rank (world ranks r % S + S*i) sums its slices into
+    the group's first member with ncclReduce, the complex slice viewed as
+    float64 (an entrywise sum of real and imaginary parts).  NCCL picks the
+    summation order, so float results agree with the canonical-order reference
+    within rounding (integer-valued payloads stay exact); "peer" is the
+    bitwise path.  Collective over the whole world (every rank creates every
+    group's communicator)."""
+    if world.size // s == 1:
+        return
+    if torch.cuda.device_count() < world.size:
+        raise ConfigError("reduce='nccl' needs one GPU per rank (NCCL rejects ranks sharing a device)")
+    mine = None
+    for c in range(s):
+        members = [world.world_ranks[c + s * i] for i in range(world.size // s)]
+        g = dist.new_group(members, backend="nccl")
+        if world.rank % s == c:
+            mine = (g, members[0])
+    torch.cuda.current_stream(data.device).synchronize()
+    dist.reduce(torch.view_as_real(data), dst=mine[1], op=dist.ReduceOp.SUM, group=mine[0])
+    torch.cuda.current_stream(data.device).synchronize()
+    world.barrier()
 
 
 # ---------------------------------------------------------------------------
@@ -852,7 +882,10 @@ def _rank_main(cfg: ExperimentConfig, world: Control, r: int, device: torch.devi
     torch.cuda.synchronize(device)
     world.barrier()
 
-    reduce_sum(pos_group, eng.slice.data, root=0)
+    if cfg.reduce == "nccl":
+        reduce_sum_nccl(world, cfg.subring_size, eng.slice.data)
+    else:
+        reduce_sum(pos_group, eng.slice.data, root=0)
 
     tensor = None
     if cfg.gather:

@@ -235,3 +235,15 @@ def test_fused_ring_multi_plane_share(kw):
                                                                                  else 1e-5)
     for rr in range(c.world_size):
         assert rep.meas_counts[rr] == c.subring_size * c.measurements * c.lanes
+
+
+def test_nccl_cross_subring_reduce():
+    """north_star item 4: the final cross-sub-ring reduce as ncclReduce (one GPU
+    per rank; skipped on a one-GPU box, where NCCL rejects ranks sharing a
+    device): integer payloads sum exactly in any order."""
+    import torch
+    if torch.cuda.device_count() < 4:
+        pytest.skip("needs 4 GPUs (one per rank)")
+    c = cfg(world_size=4, subring_size=2, lanes=2, measurements=3, reduce="nccl")
+    rep = E.run_experiment(c)
+    assert np.array_equal(rep.tensor, oracle_of(c))
