@@ -18,11 +18,23 @@
 //   WG3 producer (1 active lane, 24 registers): streams both TMA boxes of every
 //     walker of every tile into an NST-stage ring, running ahead across tile
 //     boundaries (no pipeline drain or refill between tiles).
+//   Edge chunks (row segments that wrap at N, a partial last column strip)
+//     are not one tensor-map box: every lane adds its own entries there
+//     (red.global), keeping those drains as short as the interior ones.
+//   The CTA's last tile is written back by the consumers themselves from the
+//     then-idle stages.
+//   Launched with programmatic dependent launch: the prologue (barrier init,
+//     TMEM alloc, L2 prefetch of the first boxes) overlaps the previous
+//     kernel's tail; payload loads and slice updates wait for it
+//     (griddepcontrol.wait).
+//   EXACT = true: G4_ARITH_EXACT in the same structure (block loaded at tile
+//     start, reference op order, TMA stores) -- selectable (G4RING_V3_EXACT),
+//     measured slower than geometry 13.
 // What this removes against v2 (geometry 25, one 4-warp tile per CTA, 4096
 // CTAs): the per-CTA prologue (barrier init, first fills landing) and epilogue
 // (park + bulk reduce + waiting for it to read) on every tile, and one of the
 // two CTAs per SM sitting in them; and the CTA tile doubles (8 consumer warps),
-// cutting the TMA fill bytes per update from 7.75 to 5.9 B.
+// cutting the TMA fill bytes per update from 7.75 to 5.9 B.  DESIGN.md §4.
 #include <algorithm>
 #include <cstring>
 #include <mutex>
@@ -100,28 +112,6 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
           "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
         : "r"(taddr)
         : "memory");
-}
-// A parked chunk (DD row segments of 32 entries, slice plane `plane`, rows k1b + d,
-// columns k2b + d + i for the valid columns j0 + i < N) added segment by segment:
-// rows past N skipped, columns split at the row end.  Edge tiles only (one lane).
-// Inlined: an ABI call from a setmaxnreg-reduced warp group may use registers the
-// group no longer owns (a __noinline__ version corrupted the edge chunks).
-template <bool ADD = true>
-__device__ __forceinline__ void pst_edge_chunk(const TmaParams<double>& P, int plane, int k1b, int k2b, int j0, int dd,
-                                            const Cx<double>* park) {
-    const int n = P.n;
-    Cx<double>* base = P.g4 + (int64_t)plane * n * n;
-    const int cnt = min(32, n - j0);
-    for (int d = 0; d < dd; ++d) {
-        const int k1 = k1b + d;  // < 2N
-        if (k1 >= n) break;
-        int k2 = k2b + d;
-        if (k2 >= n) k2 -= n;
-        Cx<double>* row = base + (int64_t)k1 * n;
-        const int run1 = min(cnt, n - k2);
-        segment_out<ADD, double>(row + k2, park + d * 32, run1);
-        if (run1 < cnt) segment_out<ADD, double>(row, park + d * 32 + run1, cnt - run1);
-    }
 }
 // Lab timeline (G4RING_V3_TRACE): row 31 of a CTA's trace holds %globaltimer
 // stamps (ns, comparable across SMs): 0 CTA entry, 1 first payload landed,
@@ -542,25 +532,19 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             __syncwarp();
             if (lane == 0) {
                 pdl_wait();  // the previous kernel's slice updates land first
-                const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
-                const int k1b = t.k1_0 + e0;
-                const bool box = P.use_gmap && k1b + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n;
-                const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
+                // (an interior block: edge blocks took the per-lane path above)
+                const int np = min(PP, (int)(P.hi - P.lo) - p_lo_d);
                 for (int p = 0; p < np; ++p) {
-                    if (box && EXACT)
+                    if (EXACT)
                         asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group"
                                      " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&P.gmap)),
-                                     "r"(park + p * G::CHUNK_BYTES), "r"(2 * (t.j0 - t.k1_0 + n)), "r"(k1b),
-                                     "r"(p_lo + p) : "memory");
-                    else if (box)
+                                     "r"(park + p * G::CHUNK_BYTES), "r"(2 * (t.j0 - t.k1_0 + n)), "r"(k1b_d),
+                                     "r"(p_lo_d + p) : "memory");
+                    else
                         asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group"
                                      " [%0, {%2, %3, %4}], [%1];" ::"l"(reinterpret_cast<uint64_t>(&P.gmap)),
-                                     "r"(park + p * G::CHUNK_BYTES), "r"(2 * (t.j0 - t.k1_0 + n)), "r"(k1b),
-                                     "r"(p_lo + p) : "memory");
-                    else
-                        pst_edge_chunk<!EXACT>(P, p_lo + p, k1b, t.j0 + e0, t.j0, DD,
-                                       reinterpret_cast<const Cx<double>*>(smem_raw + (park + p * G::CHUNK_BYTES -
-                                                                                       smem_u32(smem_raw))));
+                                     "r"(park + p * G::CHUNK_BYTES), "r"(2 * (t.j0 - t.k1_0 + n)), "r"(k1b_d),
+                                     "r"(p_lo_d + p) : "memory");
                 }
                 asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                 asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // park read before exit

@@ -11,8 +11,9 @@ for tool in memcheck racecheck synccheck; do
     run "G4RING_V2GEOM=25" "--n 128 --planes 32 --batch 6 --arith $a" "geom 25"
     run "G4RING_V2GEOM=27" "--n 128 --planes 16 --batch 6 --arith $a" "geom 27"
   done
-  for g in 40 43; do for h in 0 131072; do
+  for g in 40 43; do for h in 0; do
     run "G4RING_V2GEOM=$g G4RING_V3_HINTS=$h" "--n 160 --planes 40 --batch 6 --arith fused" "v3 geom $g hints $h"
-    run "G4RING_V2GEOM=$g G4RING_V3_HINTS=$h" "--n 128 --planes 32 --batch 5 --dtype mixed --arith fused" "v3 geom $g hints $h"
+    run "G4RING_V2GEOM=$g G4RING_V3_HINTS=$h" "--n 128 --planes 32 --batch 9 --dtype mixed --arith fused" "v3 geom $g hints $h"
+    run "G4RING_V2GEOM=$g" "--n 200 --planes 40 --batch 8 --arith exact" "v3 exact geom $g"
   done; done
 done
