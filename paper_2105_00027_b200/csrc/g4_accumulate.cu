@@ -798,6 +798,11 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 40:
         case 42:
         case 43:
+        case 45:  // v3 for complex64 slices: fused + deferred
+            if constexpr (FUSED && sizeof(R) == 4 && sizeof(RG) == 4)
+                return launch_pst32(g, prm.g4, prm.lo, prm.hi, prm.n, reinterpret_cast<const void* const*>(prm.stg),
+                                    prm.nbatch, st);
+            return launch_v2_geom<R, RG, FUSED>(FUSED ? 12 : 13, prm, st);
         case 44:  // v3, the persistent kernel (complex128 slices): fused + deferred, or exact
             if constexpr (sizeof(R) == 8)
                 return launch_pst<RG>(g, !FUSED, prm.g4, prm.lo, prm.hi, prm.n,
@@ -837,7 +842,8 @@ static bool geom_info(int g, GeomInfo* out) {
         case 40:
         case 42:
         case 43:
-        case 44: {
+        case 44:
+        case 45: {
             int pp, dd, q, dr, nst;
             pst_geom_info(g, &pp, &dd, &q, &dr, &nst);
             *out = {pp, dd, q, dr, nst, 1, 16};
@@ -872,8 +878,11 @@ static int v2_geom(int n, int64_t planes, bool deferred, bool c64_slice, int nba
     // geometry 12 (the producer warp group loses there, lab35).
     // With few walkers per pass the persistent kernel's fixed hand-off and
     // slice reduction per tile dominate: geometry 25 below V3_MIN_WALKERS.
-    if (c64_slice) return 12;
     static const int v3_min = env_int("G4RING_V3_MIN_WALKERS", 8);
+    if (c64_slice) {  // complex64 slices: geometry 12, or v3's complex64 kernel (G4RING_V3_C64=1)
+        static const int v3_c64 = env_int("G4RING_V3_C64", 0);
+        return (v3_c64 && nbatch >= v3_min) ? 45 : 12;
+    }
     if (nbatch < v3_min) return 25;
     return n > 2048 ? 43 : 40;
 }

@@ -133,8 +133,8 @@ struct V3Tile {
     int64_t q0;
     int k1_0, j0;
 };
-template <class G>
-__device__ __forceinline__ V3Tile v3_tile(const TmaParams<double>& P, int lin) {
+template <class G, typename R>
+__device__ __forceinline__ V3Tile v3_tile(const TmaParams<R>& P, int lin) {
     const int n = P.n;
     const TileCoord tc = tile_coord((unsigned)lin, P.nx, (n + 31) / 32, (n + G::DR - 1) / G::DR);
     return {P.lo + (int64_t)tc.x * G::Q, tc.z * G::DR, tc.y * 32};
@@ -672,6 +672,288 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
 //   40: 8x4 blocks, 2x4 warps (tile 16 planes x 16 diagonals), 4 stages, 4 park slots
 //   (a 32 x 8 tile, 4x2 warps, needs a band of 39 rows + 32 columns: beyond the staged halo)
 //   42: as 40 with 3 stages and 8 park slots; 43: 3 stages, 10 park slots; 44: 2 stages, 16 park slots
+// ---------------------------------------------------------------------------
+// K1 v3 for complex64 slices (fused, deferred): the same producer and
+// consumer roles with float accumulators; a 32-entry block is 64 TMEM columns,
+// so four hand-off buffers fit.  The epilogue has no park: complex64 row
+// segments cannot be sheared tensor-map boxes (the (N+1)-entry row stride is not
+// a 16-B multiple), so every lane adds its own entries with one
+// red.global.add.v2.f32 each (a warp's row segment is one coalesced 256-B run,
+// split at the row end).  The last tile goes out the same way from the
+// consumers' registers.
+constexpr int V3C64_BUFS = 4;
+
+__device__ __forceinline__ void edge_entry32(const TmaParams<float>& P, int plane, int k1, int k2, int c, float re,
+                                             float im) {
+    const int n = P.n;
+    if (k1 >= n || c >= n) return;
+    if (k2 >= n) k2 -= n;
+    float* g = reinterpret_cast<float*>(P.g4 + ((int64_t)plane * n + k1) * n + k2);
+    asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(g), "f"(re), "f"(im) : "memory");
+}
+
+template <class G>
+struct V3C64Smem {  // stages, then the barriers (no park)
+    static constexpr uint32_t BAR_OFF = G::NST * G::STAGE_BYTES;
+    static constexpr size_t SMEM = BAR_OFF + (2 * G::NST + 2 * V3C64_BUFS) * sizeof(uint64_t) + 16;
+    static_assert(SMEM <= 227 * 1024, "v3 c64 stages exceed shared memory");
+};
+
+template <class G>
+__global__ void __launch_bounds__(512, 1) k_accumulate_pst32(const __grid_constant__ TmaParams<float> P) {
+    using R = float;
+    using RG = float;
+    constexpr int PP = G::PP, DD = G::DD, NST = G::NST, DR = G::DR, NB = V3C64_BUFS;
+    constexpr int EW = G::ES / 8;
+    constexpr int COLS = PP * DD * 2;  // TMEM columns of one consumer block
+    static_assert(PP * DD == 32 && 2 * NB * COLS == 512, "four 2-warp buffers per lane quarter");
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + V3C64Smem<G>::BAR_OFF);
+    uint64_t* empty = full + NST;
+    uint64_t* tfull = empty + NST;
+    uint64_t* tready = tfull + NB;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + NB);
+
+    const int n = P.n;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = P.nx * ((n + 31) / 32) * ((n + DR - 1) / DR);
+    const int my_tiles = v3_count(ntiles);
+    const int nb = P.nbatch;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NST; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], G::CW);
+        }
+        for (int b = 0; b < NB; ++b) {
+            mbar_init(&tfull[b], G::CW);
+            mbar_init(&tready[b], 4);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    }
+    if (warp == 8) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp >= 12) {
+        // ---------------- producer (as the complex128 kernel) ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_PRODUCER) : "memory");
+        if (threadIdx.x == 384) {
+            pdl_wait();
+            int it = 0;
+            for (int k = 0; k < my_tiles; ++k) {
+                const V3Tile t = v3_tile<G>(P, v3_lin(k));
+                const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
+                const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
+                const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
+                const int pd = xd & 1, ps = xs & 1;
+                for (int w = 0; w < nb; ++w, ++it) {
+                    const int s = it % NST;
+                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
+                    unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
+                    tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s]);
+                    tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
+                }
+            }
+        }
+        __syncwarp();
+        return;
+    }
+
+    if (warp >= 8) {
+        // ---------------- epilogue: TMEM -> one red.global.add.v2.f32 per entry ----------------
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_EPILOGUE) : "memory");
+        const int q = warp - 8;
+        const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
+        pdl_wait();
+        for (int k = 0; k < my_tiles - 1; ++k) {  // the last tile: consumers
+            const int b = k % NB;
+            mbar_wait(&tfull[b], (k / NB) & 1);
+            tc_fence_after();
+            const V3Tile t = v3_tile<G>(P, v3_lin(k));
+#pragma unroll 1
+            for (int h = 0; h < 2; ++h) {
+                const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
+                const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
+                const int e0 = DD * wr;
+                const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
+#pragma unroll 1
+                for (int c = 0; c < 2; ++c) {  // 16 entries (planes 4c .. 4c + 3) per load
+                    uint32_t v[32];
+                    tmem_ld32(tq + b * (2 * COLS) + h * COLS + c * 32, v);
+                    tmem_wait_ld();
+#pragma unroll
+                    for (int i = 0; i < 16; ++i) {
+                        const int e = 16 * c + i, p = e / DD, d = e % DD;
+                        if (p < np)
+                            edge_entry32(P, p_lo + p, t.k1_0 + e0 + d, t.j0 + e0 + d + lane, t.j0 + lane,
+                                         __uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tready[b]);
+        }
+        asm volatile("barrier.sync 1, 128;" ::: "memory");
+        if (warp == 8) {
+            tc_fence_after();
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+        }
+        return;
+    }
+
+    // ---------------- consumers ----------------
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(V3_REG_CONSUMER) : "memory");
+    const int wq = warp % G::CWQ, wr = warp / G::CWQ;
+    const int e0 = DD * wr;
+    const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (warp >> 2) * COLS;
+    int it = 0;
+    for (int k = 0; k < my_tiles; ++k) {
+        const V3Tile t = v3_tile<G>(P, v3_lin(k));
+        const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
+        const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
+        const int pd = (t.j0 - t.k1_0 + P.off) & 1;
+        const int ps = (C0 - R0 + P.off) & 1;
+        const int sh_o = (PP * wq + DR - DD - e0) * G::W + (31 - lane) + ps;
+        const int dr_o = e0 * G::W + lane + pd;
+        Cx<R> acc[PP][DD];
+#pragma unroll
+        for (int p = 0; p < PP; ++p)
+#pragma unroll
+            for (int d = 0; d < DD; ++d) acc[p][d].re = acc[p][d].im = R(0);
+#pragma unroll 1
+        for (int w = 0; w < nb; ++w, ++it) {
+            const int s = it % NST;
+            mbar_wait(&full[s], (it / NST) & 1);
+            const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
+            const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
+            const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
+            const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
+            Stg<R> dv[DD];
+#pragma unroll
+            for (int d = 0; d < DD; ++d) dv[d] = lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o);
+            constexpr int NJ = PP + DD - 1;
+            Stg<R> S = lds_plain(sh_u + sh_o, sh_d + sh_o);
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) {
+                Stg<R> Sn;
+                if (j + 1 < NJ) Sn = lds_plain(sh_u + sh_o + (j + 1) * G::W, sh_d + sh_o + (j + 1) * G::W);
+#pragma unroll
+                for (int d = 0; d < DD; ++d) {
+                    const int p = j + d - (DD - 1);
+                    if (p < 0 || p >= PP) continue;
+                    update_fused(acc[p][d], S, dv[d]);
+                }
+                if (j + 1 < NJ) S = Sn;
+            }
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[s]);
+        }
+        if (k == my_tiles - 1) {  // the last tile: straight from the registers
+            pdl_wait();
+            const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
+            const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
+#pragma unroll
+            for (int p = 0; p < PP; ++p)
+#pragma unroll
+                for (int d = 0; d < DD; ++d)
+                    if (p < np)
+                        edge_entry32(P, p_lo + p, t.k1_0 + e0 + d, t.j0 + e0 + d + lane, t.j0 + lane, acc[p][d].re,
+                                     acc[p][d].im);
+            break;
+        }
+        const int b = k % NB;
+        if (k >= NB) mbar_wait(&tready[b], ((k / NB) - 1) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            uint32_t v[32];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+                const Cx<R>& a = acc[(16 * c + i) / DD][(16 * c + i) % DD];
+                v[2 * i] = __float_as_uint(a.re);
+                v[2 * i + 1] = __float_as_uint(a.im);
+            }
+            tmem_st32(tq + b * (2 * COLS) + c * 32, v);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tfull[b]);
+    }
+}
+
+template <class G>
+static g4_status launch_pst32_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                                int32_t nbatch, cudaStream_t st) {
+    auto kern = k_accumulate_pst32<G>;
+    constexpr size_t SMEM = V3C64Smem<G>::SMEM;
+    int dev = 0;
+    G4_CUDA(cudaGetDevice(&dev));
+    {
+        static std::mutex mu;
+        static uint64_t done = 0;
+        std::lock_guard<std::mutex> lk(mu);
+        if (!(done & (1ull << (dev & 63)))) {
+            G4_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+            done |= 1ull << (dev & 63);
+        }
+    }
+    int sms = 0;
+    G4_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    for (int b0 = 0; b0 < nbatch; b0 += TMA_MAXW) {
+        TmaParams<float> tp;
+        std::memset(&tp, 0, sizeof(tp));
+        tp.g4 = static_cast<Cx<float>*>(g4p);
+        tp.lo = lo;
+        tp.hi = hi;
+        tp.n = n;
+        tp.off = sheared_offset(n, G::ES);
+        tp.nbatch = std::min(TMA_MAXW, nbatch - b0);
+        for (int i = 0; i < tp.nbatch; ++i) {
+            MapPair mp;
+            G4_TRY(get_maps(staged[b0 + i], n, G::ES, G::NSH, G::W, G::DR, 2, &mp));
+            tp.dmap[i] = mp.dmap;
+            tp.smap[i] = mp.smap;
+        }
+        tp.nx = (int32_t)((hi - lo + G::Q - 1) / G::Q);
+        const int64_t tiles = (int64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
+        if (tiles >= (1ll << 31)) return fail(G4_ERR_CONTRACT, "accumulate: tile count too large");
+        const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+        static const bool pdl = env_int("G4RING_PDL", 1) != 0;
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(grid);
+        lc.blockDim = dim3(G::THREADS);
+        lc.dynamicSmemBytes = SMEM;
+        lc.stream = st;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        lc.attrs = attr;
+        lc.numAttrs = pdl ? 1 : 0;
+        G4_TRY(check_cuda(cudaLaunchKernelEx(&lc, kern, tp), "k_accumulate_pst32 launch"));
+    }
+    return G4_OK;
+}
+
+g4_status launch_pst32(int geom, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                       int32_t nbatch, cudaStream_t st) {
+    switch (geom) {
+        case 45: return launch_pst32_t<V3Geom<float, 8, 4, 2, 4, 7, 4>>(g4p, lo, hi, n, staged, nbatch, st);
+        default: return fail(G4_ERR_CONTRACT, "unknown v3 complex64 geometry");
+    }
+}
+
 template <typename RG, class G>
 static g4_status launch_pst_mode(bool exact, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                                  int32_t nbatch, cudaStream_t st) {
@@ -700,6 +982,7 @@ bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst) {
         case 42: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 3; return true;
         case 43: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 3; return true;
         case 44: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 2; return true;
+        case 45: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 7; return true;
         default: return false;
     }
 }

@@ -278,5 +278,8 @@ template <typename RG>
 g4_status launch_pst(int geom, bool exact, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                      int32_t nbatch, cudaStream_t st);
 bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst);
+// K1 v3 for complex64 slices (fused, deferred; geometry 45).
+g4_status launch_pst32(int geom, void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
+                       int32_t nbatch, cudaStream_t st);
 
 }  // namespace g4
