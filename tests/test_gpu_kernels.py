@@ -384,7 +384,10 @@ def test_core_copy_plus_halo_rebuild_is_exact(cuda_dev, n, dtype):
                                               # K1 v3 (>= 8 walkers, >= 16 planes) with a partial last column
                                               # strip and row wraps (the per-lane edge path), nonzero start
                                               ("c128", 200, 5, 45, 8), ("mixed", 150, 0, 33, 12),
-                                              ("c128", 64, 0, 64, 9)])
+                                              ("c128", 64, 0, 64, 9),
+                                              # complex64 slices with >= 8 walkers (geometry 12, or v3's
+                                              # complex64 kernel under G4RING_V3_C64=1)
+                                              ("c64", 200, 0, 40, 9), ("c64", 128, 5, 37, 16)])
 def test_fused_deferred_update(oracle, cuda_dev, dtype, n, lo, hi, nb):
     """G4_ARITH_FUSED with >= 4 walkers adds the walkers' sum to a NONZERO slice
     at the end (L2 reduction): integer payloads stay bitwise, float within
