@@ -279,6 +279,9 @@ def reduce_sum(ctl: Control, data: torch.Tensor, root: int = 0) -> None:
     ctl.barrier()
 
 
+_NCCL_GROUPS: dict[tuple[int, ...], object] = {}
+
+
 def reduce_sum_nccl(world: Control, s: int, data: torch.Tensor) -> None:
     """The cross-sub-ring reduce as an NCCL collective (north_star item 4): the
     position group of this rank (world ranks r % S + S*i) sums its slices into
@@ -294,8 +297,10 @@ def reduce_sum_nccl(world: Control, s: int, data: torch.Tensor) -> None:
         raise ConfigError("reduce='nccl' needs one GPU per rank (NCCL rejects ranks sharing a device)")
     mine = None
     for c in range(s):
-        members = [world.world_ranks[c + s * i] for i in range(world.size // s)]
-        g = dist.new_group(members, backend="nccl")
+        members = tuple(world.world_ranks[c + s * i] for i in range(world.size // s))
+        g = _NCCL_GROUPS.get(members)
+        if g is None:  # communicators are created once per member set and reused by later runs
+            g = _NCCL_GROUPS[members] = dist.new_group(list(members), backend="nccl")
         if world.rank % s == c:
             mine = (g, members[0])
     torch.cuda.current_stream(data.device).synchronize()
