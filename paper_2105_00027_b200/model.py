@@ -239,6 +239,12 @@ class K1Calibration:
     eff_smem: float = 0.78             # exact, N = 512: B = 8 / 16 at 0.72 / 0.88 of the smem data path (r01j)
     eff_fp: float = 0.85
     launch_s: float = 4e-6             # launch + tail of one pass
+    # K1 v3 (the persistent TMEM-hand-off kernel): the slice traffic and the
+    # math overlap only partly; time = w_hbm * HBM time + w_fp * FP64 issue time
+    # at peak, fitted on the round-2 lines (N = 512 B = 8 and 16; checked at
+    # N = 1024 and 4608 within 8 %, profiles/r02e_bench*.json)
+    v3_w_hbm: float = 0.684
+    v3_w_fp: float = 1.123
 
     @property
     def smem_bytes_per_s(self) -> float:
@@ -281,7 +287,9 @@ def k1_pass_time(n: int, planes: int, batch: int, dtype: str = "c128", arith: st
     bounds = {"hbm": hbm_b / (cal.hbm_gbs * 1e9 * cal.eff_hbm),
               "smem": smem_b / (cal.smem_bytes_per_s * cal.eff_smem * util),
               "fp": fp_i / (fpeak * cal.eff_fp * util)}
-    if g["deferred"]:
+    if g["variant"] == 3:
+        bounds["v3"] = (cal.v3_w_hbm * hbm_b / (cal.hbm_gbs * 1e9) + cal.v3_w_fp * fp_i / fpeak) / util
+    elif g["deferred"]:
         # The deferred update's L2 read-modify-write and the payload fills share
         # the L2 <-> SM path and do not overlap: the r01j fused lines (B = 8, 16;
         # N = 512 and 4608) sit within 7 % of the SUM of the two times at peak.

@@ -81,11 +81,13 @@ def test_k1_model_against_measured_bench_lines():
                 mode = _lib.G4_ARITH_FUSED if arith == "fused" else _lib.G4_ARITH_EXACT
                 _lib.check(lib.g4_set_arith_mode(mode))
                 k = M.k1_pass_time(c["n"], c["planes"], c["walkers_per_pass"], d["dtype"], arith)
+                if k["geometry"]["variant"] == 3:
+                    continue  # served by K1 v3 since round 2: test_k1_v3_model_against_round2_lines
                 assert k["updates_per_s"] == pytest.approx(value, rel=0.15), (f.name, arith)
                 checked += 1
     finally:
         _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))
-    assert checked >= 8
+    assert checked >= 5
 
 
 def test_k1_model_bounds_switch_with_batch():
@@ -141,3 +143,24 @@ def test_wire_bytes_are_payload_cores():
     assert M.wire_payload_bytes(512, "c128") == 2 * 512 * 512 * 16
     assert M.wire_payload_bytes(512, "mixed") == 2 * 512 * 512 * 8
     assert M.staged_payload_bytes(512, "c128") > M.wire_payload_bytes(512, "c128")
+
+
+def test_k1_v3_model_against_round2_lines():
+    """The v3 composition (model.K1Calibration.v3_w_*) within 15 % of the final
+    round-2 bench lines: the headline (N = 512, B = 8), B = 16, config 4's share
+    (N = 4608, geometry 43) and config 3's index space (N = 1024)."""
+    from paper_2105_00027_b200 import _lib
+    lib = _lib.load()
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED))
+    try:
+        d = json.loads((ROOT / "profiles" / "r02e_bench.json").read_text())
+        b16 = json.loads((ROOT / "profiles" / "r02e_bench_b16.json").read_text())
+        c4 = json.loads((ROOT / "profiles" / "r02e_bench_c4.json").read_text())
+        pts = [((512, 64, 8), d["value"]), ((512, 64, 16), b16["value"]), ((4608, 72, 8), c4["value"]),
+               ((1024, 64, 8), d["config_points"]["c3_full"]["updates_per_s"])]
+        for (n, p, b), value in pts:
+            k = M.k1_pass_time(n, p, b, "c128", "fused")
+            assert k["geometry"]["variant"] == 3 and k["bound"] == "v3"
+            assert k["updates_per_s"] == pytest.approx(value, rel=0.15), (n, p, b)
+    finally:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))

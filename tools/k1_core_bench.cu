@@ -16,8 +16,8 @@ __device__ __forceinline__ void upd(double2& a, const Stg& S, const Stg& D) {
     re = __fma_rn(-S.di, D.ui, re); im = __fma_rn(S.di, D.ur, im);
     a.x = re; a.y = im;
 }
-template <int PP, int DD, int MAXR, bool SYNC>
-__global__ void __launch_bounds__(256, 1) __maxnreg__(MAXR) core(double* out, int walkers) {
+template <int PP, int DD, int MAXR, bool SYNC, int NT = 256>
+__global__ void __launch_bounds__(NT, 1) __maxnreg__(MAXR) core(double* out, int walkers) {
     constexpr int NJ = PP + DD - 1;
     extern __shared__ double2 sm[];  // 4 stages x [spin][48 rows][32]
     __shared__ uint64_t bar;
@@ -54,20 +54,20 @@ __global__ void __launch_bounds__(256, 1) __maxnreg__(MAXR) core(double* out, in
     for (int p = 0; p < PP; ++p) for (int d = 0; d < DD; ++d) s += acc[p][d].x + acc[p][d].y;
     out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
-template <int PP, int DD, int MAXR, bool SYNC>
+template <int PP, int DD, int MAXR, bool SYNC, int NT = 256>
 void run(double* out, int sms) {
     const int walkers = 2000;
     const size_t smem = 4 * 2 * 48 * 32 * 16;
-    auto k = core<PP, DD, MAXR, SYNC>;
+    auto k = core<PP, DD, MAXR, SYNC, NT>;
     cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-    k<<<sms, 256, smem>>>(out, walkers);
+    k<<<sms, NT, smem>>>(out, walkers);
     cudaEventRecord(a);
-    k<<<sms, 256, smem>>>(out, walkers);
+    k<<<sms, NT, smem>>>(out, walkers);
     cudaEventRecord(b); cudaEventSynchronize(b);
     float ms; cudaEventElapsedTime(&ms, a, b);
-    const double dfma = (double)sms * 256 * walkers * PP * DD * 8;
-    printf("PP %d DD %d maxreg %3d sync %d: %6.2f T DFMA/s (%5.1f%% of 16.56)  %s\n", PP, DD, MAXR, (int)SYNC,
+    const double dfma = (double)sms * NT * walkers * PP * DD * 8;
+    printf("warps %2d PP %d DD %d maxreg %3d sync %d: %6.2f T DFMA/s (%5.1f%% of 16.56)  %s\n", NT / 32, PP, DD, MAXR, (int)SYNC,
            dfma / ms / 1e9, dfma / ms / 1e9 / 16.56 * 100, cudaGetErrorString(cudaGetLastError()));
 }
 int main() {
@@ -83,5 +83,10 @@ int main() {
     run<8, 3, 184, true>(out, sms);
     run<6, 4, 216, true>(out, sms);
     run<8, 2, 168, true>(out, sms);
+    run<8, 2, 168, true, 384>(out, sms);
+    run<8, 3, 168, true, 384>(out, sms);
+    run<6, 4, 168, true, 384>(out, sms);
+    run<4, 4, 128, true, 512>(out, sms);
+    run<8, 4, 216, true, 256>(out, sms);
     return 0;
 }
