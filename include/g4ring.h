@@ -134,6 +134,9 @@ g4_status g4_set_kernel_variant(int32_t variant);
  *     bitwise for integer-valued payloads, ~1.5x fewer FP64 issues. */
 typedef enum { G4_ARITH_EXACT = 0, G4_ARITH_FUSED = 1 } g4_arith_mode;
 g4_status g4_set_arith_mode(int32_t mode);
+/* The current K1 arithmetic mode (G4_ARITH_EXACT or G4_ARITH_FUSED), e.g. to
+ * restore it after a temporary change. */
+int32_t g4_get_arith_mode(void);
 
 /* The K1 configuration g4_accumulate_staged would launch for this shape under
  * the current arithmetic mode (host only, no GPU needed), for measurement and

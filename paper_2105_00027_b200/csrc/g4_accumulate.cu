@@ -994,6 +994,8 @@ g4_status g4_k1_config(int32_t n, int64_t planes, int32_t nbatch, int32_t dtype,
     return G4_OK;
 }
 
+int32_t g4_get_arith_mode(void) { return g4::g_arith; }
+
 g4_status g4_set_arith_mode(int32_t mode) {
     if (mode != G4_ARITH_EXACT && mode != G4_ARITH_FUSED)
         return g4::fail(G4_ERR_CONTRACT, "arith mode must be G4_ARITH_EXACT or G4_ARITH_FUSED");

@@ -254,12 +254,19 @@ class K1Calibration:
 B200_K1 = K1Calibration()
 
 
-def k1_geometry(n: int, planes: int, dtype: str, nbatch: int = 8) -> dict:
-    """The launch g4_accumulate_staged picks for this shape under the current
-    arithmetic mode (g4_k1_config)."""
+def k1_geometry(n: int, planes: int, dtype: str, nbatch: int = 8, arith: str | None = None) -> dict:
+    """The launch g4_accumulate_staged picks for this shape (g4_k1_config), under
+    the given arithmetic mode ("exact" / "fused"), or the library's current one."""
     _check_dtype(dtype)
+    lib = _lib.load()
     out = (ctypes.c_int32 * 9)()
-    _lib.check(_lib.load().g4_k1_config(n, planes, nbatch, _DTYPE[dtype], out), "k1_config")
+    prev = lib.g4_get_arith_mode()
+    if arith is not None:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if arith == "fused" else _lib.G4_ARITH_EXACT))
+    try:
+        _lib.check(lib.g4_k1_config(n, planes, nbatch, _DTYPE[dtype], out), "k1_config")
+    finally:
+        _lib.check(lib.g4_set_arith_mode(prev))
     v = list(out)
     return {"variant": v[0], "pp": v[1], "dd": v[2], "q": v[3], "dr": v[4], "stages": v[5],
             "ctas_per_sm": v[6], "warps": v[7], "deferred": bool(v[8])}
@@ -270,7 +277,7 @@ def k1_pass_time(n: int, planes: int, batch: int, dtype: str = "c128", arith: st
     """Modelled time of one K1 launch (B walkers over a P-plane slice) and its bounds."""
     if min(n, planes, batch) < 1:
         raise ContractViolation("k1_pass_time arguments must be >= 1")
-    g = k1_geometry(n, planes, dtype, batch)
+    g = k1_geometry(n, planes, dtype, batch, arith)
     eb, peb = entry_bytes(dtype), payload_entry_bytes(dtype)
     upd = batch * planes * n * n
     hbm_b = 2 * planes * n * n * eb + batch * 2 * n * n * peb
