@@ -314,6 +314,7 @@ def run_gpu(args):
         t_end.record(stream)
         torch.cuda.synchronize()
     total_ms = t_start.elapsed_time(t_end)
+    launched_geom = int(lib.g4_last_k1_geometry())
     k_ms = [total_ms / args.steps]
     upd_step = B * planes * n * n
     value = upd_step * args.steps / (total_ms * 1e-3)
@@ -340,6 +341,7 @@ def run_gpu(args):
                      "peak_source": peak_kind, "kernel": "k_accumulate",
                      "bytes_per_launch": alg_bytes},
         "onchip": onchip_bounds(lib, n, planes, args.dtype, args.arith, B, upd_step / (statistics.mean(k_ms) * 1e-3)),
+        "launched_k1_geometry": launched_geom,  # g4_last_k1_geometry() after the timed region (40/43 = K1 v3)
         "clocks": clk.summary(),
         "e2e": e2e,
         "parity_check": parity,

@@ -137,6 +137,10 @@ g4_status g4_set_arith_mode(int32_t mode);
 /* The current K1 arithmetic mode (G4_ARITH_EXACT or G4_ARITH_FUSED), e.g. to
  * restore it after a temporary change. */
 int32_t g4_get_arith_mode(void);
+/* The geometry id of the last K1 launch in this process (1 = v1; 12/13/19/25 =
+ * v2 kernels; 40-45 = v3), for tests that pin the dispatch to the kernel
+ * g4_k1_config reports. */
+int32_t g4_last_k1_geometry(void);
 
 /* The K1 configuration g4_accumulate_staged would launch for this shape under
  * the current arithmetic mode (host only, no GPU needed), for measurement and

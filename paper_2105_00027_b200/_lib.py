@@ -44,6 +44,7 @@ SIGNATURES = {
     "g4_set_kernel_variant": (_i32, [_i32]),
     "g4_set_arith_mode": (_i32, [_i32]),
     "g4_get_arith_mode": (_i32, []),
+    "g4_last_k1_geometry": (_i32, []),
     "g4_k1_config": (_i32, [_i32, _i64, _i32, _i32, ctypes.POINTER(_i32)]),
     "g4_accumulate_workspace_bytes": (_i64, [_i32, _i32, _i32]),
     "g4_accumulate": (_i32, [_vp, _i64, _i64, _i32, _vpp, _vpp, _i32, _i32, _i32, _vp, _i64, _vp]),

@@ -37,6 +37,7 @@
 //    stored (exact) or added in L2 (fused, deferred update).  Geometry choice
 //    and the measured alternatives: launch_v2_geom below, DESIGN.md section 4.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -763,8 +764,13 @@ static g4_status launch_v2(const AccParams<R, RG>& prm, cudaStream_t st) {
 //   default for P >= 16 (-4 % at B = 8 and 16, lab35).  27: geometry 19 likewise
 //   (3 CTAs/SM, consumers at 136): within 2 % of 19 at P = 8, B = 8 (lab36);
 //   selectable only.
+// The geometry id of the last K1 launch (v1: 1), for tests that pin the
+// dispatch: g4_last_k1_geometry().
+static std::atomic<int> g_last_geom{0};
+
 template <typename R, typename RG, bool FUSED>
 static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t st) {
+    g_last_geom.store(g, std::memory_order_relaxed);  // a fallback below re-enters with its own id
     switch (g) {
         case 0: return launch_v2<R, RG, V2Geom<RG, 4, 4, 3>, FUSED, 3>(prm, st);
         case 3: return launch_v2<R, RG, V2Geom<RG, 4, 4, 2>, FUSED, 4>(prm, st);
@@ -795,14 +801,14 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 24: return launch_v2<R, RG, V2Geom<RG, 8, 2, 2, 2, 2, 1, 2>, FUSED, 4>(prm, st);
         case 25: return launch_v2<R, RG, V2Geom<RG, 8, 2, 3, 4, 2, 1, 1, 1>, FUSED, 2>(prm, st);
         case 27: return launch_v2<R, RG, V2Geom<RG, 8, 1, 2, 2, 4, 1, 1, 1>, FUSED, 3>(prm, st);
-        case 40:
-        case 42:
-        case 43:
         case 45:  // v3 for complex64 slices: fused + deferred
             if constexpr (FUSED && sizeof(R) == 4 && sizeof(RG) == 4)
                 return launch_pst32(g, prm.g4, prm.lo, prm.hi, prm.n, reinterpret_cast<const void* const*>(prm.stg),
                                     prm.nbatch, st);
             return launch_v2_geom<R, RG, FUSED>(FUSED ? 12 : 13, prm, st);
+        case 40:
+        case 42:
+        case 43:
         case 44:  // v3, the persistent kernel (complex128 slices): fused + deferred, or exact
             if constexpr (sizeof(R) == 8)
                 return launch_pst<RG>(g, !FUSED, prm.g4, prm.lo, prm.hi, prm.n,
@@ -900,6 +906,7 @@ static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
             v2_geom(prm.n, planes, FUSED && defer_update(prm.nbatch, planes), sizeof(R) == 4,
                     std::min<int32_t>(prm.nbatch, TMA_MAXW)),
             prm, st);
+    g_last_geom.store(1, std::memory_order_relaxed);
     if (planes <= 4) return launch_v1<R, RG, 4, 4, 1, 12, FUSED>(prm, st);
     if (planes <= 8) return launch_v1<R, RG, 4, 4, 2, 6, FUSED>(prm, st);
     return launch_v1<R, RG, 4, 4, 4, 3, FUSED>(prm, st);
@@ -995,6 +1002,8 @@ g4_status g4_k1_config(int32_t n, int64_t planes, int32_t nbatch, int32_t dtype,
 }
 
 int32_t g4_get_arith_mode(void) { return g4::g_arith; }
+
+int32_t g4_last_k1_geometry(void) { return g4::g_last_geom.load(std::memory_order_relaxed); }
 
 g4_status g4_set_arith_mode(int32_t mode) {
     if (mode != G4_ARITH_EXACT && mode != G4_ARITH_FUSED)

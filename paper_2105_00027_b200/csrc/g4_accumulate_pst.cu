@@ -435,10 +435,13 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
 #pragma unroll
                 for (int d = 0; d < DD; ++d) acc[p][d].re = acc[p][d].im = R(0);
         }
+        long long fill_wait = 0;  // lab trace: cycles warp 0 waited for fills in this tile
 #pragma unroll 1
         for (int w = 0; w < nb; ++w, ++it) {
             const int s = it % NST;
+            const long long fw0 = P.trace ? clock64() : 0;
             mbar_wait(&full[s], (it / NST) & 1);
+            if (P.trace) fill_wait += clock64() - fw0;
             if (it == 0 && warp == 0 && lane == 0) trace_gt(P.trace, 1);
             const Cx<RG>* dir_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::DIR_OFF);
             const Cx<RG>* dir_d = dir_u + G::DIR_ELEMS;
@@ -574,8 +577,10 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             tmem_st32(tq + b * 256 + c * 32, v);
         }
         }
-        if (P.trace && k < 31 && lane == 0 && (warp == 0 || warp == 7))
-            P.trace[((size_t)blockIdx.x * 32 + k) * 8 + (warp == 0 ? 2 : 5)] = clock64();
+        if (P.trace && k < 31 && lane == 0 && warp == 0) {
+            P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 2] = clock64();
+            P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 5] = fill_wait;
+        }
         pend = b;  // announced after the next tile's first walker (or below)
         if (last) {
             tmem_wait_st();

@@ -457,3 +457,33 @@ def test_cluster_multicast_geometry_parity():
                        capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert r.stdout.count(" ok") == 24
+
+
+@pytest.mark.parametrize("arith,dtype,n_k,n_w,planes,nb,geom", [
+    ("fused", "c128", 16, 32, 64, 8, 40),    # the headline: K1 v3
+    ("fused", "mixed", 16, 32, 64, 8, 40),
+    ("fused", "c128", 48, 48, 16, 8, 43),    # N > 2048: v3 with 10 park slots
+    ("fused", "c128", 16, 32, 64, 5, 25),    # 4-7 walkers: geometry 25
+    ("fused", "c128", 16, 32, 64, 2, 13),    # < 4 walkers: the exact kernel
+    ("exact", "c128", 16, 32, 64, 8, 13),
+    ("fused", "c64", 16, 32, 64, 8, 12),
+    ("fused", "c128", 16, 32, 8, 8, 19),     # the 8-GPU share of config 2
+    ("exact", "c128", 16, 32, 2, 8, 1),      # v1
+])
+def test_dispatch_launches_the_reported_kernel(cuda_dev, arith, dtype, n_k, n_w, planes, nb, geom):
+    """The kernel a launch actually runs (g4_last_k1_geometry) is the one the
+    selection table names -- a dispatch slip would stay
+    invisible to the parity tests, which every kernel passes."""
+    lib = _lib.load()
+    _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_FUSED if arith == "fused" else _lib.G4_ARITH_EXACT))
+    try:
+        sp = T.CombinedIndexSpace(n_k, n_w)
+        sdt = torch.complex64 if dtype == "c64" else torch.complex128
+        gdt = torch.complex128 if dtype == "c128" else torch.complex64
+        sl = T.GtSlice.zeros(sp, 0, planes, device=cuda_dev, dtype=sdt)
+        gs = [T.GSigma.empty(sp, device=cuda_dev, dtype=gdt) for _ in range(nb)]
+        T.accumulate_g4_batch(sl, gs)
+        torch.cuda.synchronize()
+        assert lib.g4_last_k1_geometry() == geom
+    finally:
+        _lib.check(lib.g4_set_arith_mode(_lib.G4_ARITH_EXACT))

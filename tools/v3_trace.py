@@ -44,7 +44,7 @@ def main():
     tr = raw.reshape(a.passes, grid, 32, 8)[-1].copy()  # last pass
     tr[:, 31, :] = 0  # row 31: globaltimer stamps (below)
     # [0] epi q0 tfull done, [1] epi q0 drained, [2] cons w0 tile done, [3] cons w0 tready wait,
-    # [4] cons w0 tile start, [5] cons w7 tile done, [6] epi q3 tfull done, [7] epi q3 drained
+    # [4] cons w0 tile start, [5] cons w0 fill-wait cycles, [6] epi q3 tfull done, [7] epi q3 drained
     ok = tr[:, :, 4] > 0
     ntile = ok.sum(1)
     start = np.where(ok, tr[:, :, 4], 0)
@@ -61,13 +61,13 @@ def main():
     drain = np.where(ok, tr[:, :, 1] - tr[:, :, 0], 0)[ok]
     drain3 = np.where(ok, tr[:, :, 7] - tr[:, :, 6], 0)[ok]
     lag = np.where(ok, tr[:, :, 0] - np.maximum(tr[:, :, 2], tr[:, :, 5]), 0)[ok]
-    skew = np.where(ok, tr[:, :, 5] - tr[:, :, 2], 0)[ok]
+    fillw = np.where(ok, tr[:, :, 5], 0)[ok]  # [5]: cycles consumer warp 0 waited for payload fills
     wait = tr[:, :, 3][ok]
     total = (np.max(np.where(ok, tr[:, :, 2], 0), 1) - tr[:, 0, 4])
     pct = lambda x: f"median {np.median(x):8.0f}  p90 {np.percentile(x, 90):8.0f}  max {np.max(x):8.0f}  mean {np.mean(x):8.0f}"
     print(f"grid {grid}, tiles per CTA {ntile.min()}-{ntile.max()}, CTA span (cycles): {pct(total)}")
     print(f"consumer tile (w0 start -> w0 done): {pct(dur)}")
-    print(f"w7 done - w0 done (warp skew):       {pct(skew)}")
+    print(f"w0 fill waits per tile:              {pct(fillw)}")
     print(f"epilogue start lag after w0/w7 done: {pct(lag)}")
     print(f"epilogue drain q0 (tfull -> tready):  {pct(drain)}")
     print(f"epilogue drain q3:                    {pct(drain3)}")
