@@ -46,13 +46,9 @@ namespace g4 {
 
 // Geometry: PP x DD thread block, CWQ x CWR consumer warps (CW = 8), NST
 // stages of both boxes, NPARK 2-KB park slots per epilogue warp.
-// DLDG: the direct operand comes from global memory (L2) by each consumer lane
-// (one walker ahead) instead of a TMA box, so a stage holds only the shifted
-// band and more stages fit.
-template <typename RG, int PP_, int DD_, int CWQ_, int CWR_, int NST_, int NPARK_, bool DLDG_ = false>
+template <typename RG, int PP_, int DD_, int CWQ_, int CWR_, int NST_, int NPARK_>
 struct V3Geom {
     static constexpr int PP = PP_, DD = DD_, CWQ = CWQ_, CWR = CWR_, NST = NST_, NPARK = NPARK_;
-    static constexpr bool DLDG = DLDG_;
     static constexpr int CW = CWQ * CWR;
     static_assert(CW == 8, "two consumer warp groups");
     static constexpr int THREADS = 512;                      // 4 warp groups
@@ -64,8 +60,7 @@ struct V3Geom {
     static constexpr uint32_t DIR_BYTES = 2 * DIR_ELEMS * ES;
     static constexpr uint32_t SH_BYTES = 2 * SH_ELEMS * ES;
     static constexpr uint32_t DIR_OFF = 0;
-    static constexpr uint32_t SH_OFF = DLDG ? 0 : (DIR_BYTES + 127) / 128 * 128;
-    static constexpr uint32_t FILL_BYTES = DLDG ? SH_BYTES : DIR_BYTES + SH_BYTES;  // TMA bytes per stage
+    static constexpr uint32_t SH_OFF = (DIR_BYTES + 127) / 128 * 128;
     static constexpr uint32_t STAGE_BYTES = (SH_OFF + SH_BYTES + 127) / 128 * 128;
     static constexpr uint32_t CHUNK_BYTES = DD * 32 * 16;   // one (plane, DD diagonals) chunk of the slice
     static constexpr uint32_t PARK_OFF = NST * STAGE_BYTES;
@@ -211,22 +206,6 @@ __device__ __forceinline__ void edge_entry(const TmaParams<double>& P, int plane
     }
 }
 
-// DLDG: direct operands of walker w for the warp's rows e0 .. e0 + DD - 1 of
-// tile t, lane column: stg[spin][k1_0 + e0 + d][j0 + e0 + d + lane] (the
-// staged layout's halo makes the column in range), read through L1/L2.
-template <class G>
-__device__ __forceinline__ void ldg_direct(const TmaParams<double>& P, int w, const V3Tile& t, int e0, int lane,
-                                           Stg<double> (&dv)[G::DD]) {
-    const int n = P.n;
-    const int64_t ld = staged_ld(n, 16), plane = staged_plane(n, 16);
-    const Cx<double>* b = static_cast<const Cx<double>*>(P.stg[w]);
-#pragma unroll
-    for (int d = 0; d < G::DD; ++d) {
-        const Cx<double>* u = b + (int64_t)(t.k1_0 + e0 + d) * ld + (t.j0 + e0 + d + lane);
-        dv[d] = ld_stg(u, u + plane);
-    }
-}
-
 template <typename RG, class G, bool EARLY_ST, bool EXACT>
 __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant__ TmaParams<double> P) {
     using R = double;
@@ -305,14 +284,13 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 for (int w = 0; w < nb; ++w, ++it) {
                     const int s = it % NST;
                     if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
-                    mbar_arrive_expect_tx(&full[s], G::FILL_BYTES);
+                    mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
                     unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
                     if (P.hints & 2) {
-                        if (!G::DLDG)
-                            tma_load_3d_hint(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s], keep);
+                        tma_load_3d_hint(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s], keep);
                         tma_load_3d_hint(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s], keep);
                     } else {
-                        if (!G::DLDG) tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s]);
+                        tma_load_3d(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s]);
                         tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
                     }
                 }
@@ -421,13 +399,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     const uint32_t tq = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + (warp >> 2) * G::BLOCK_COLS;
     int it = 0;
     int pend = -1;  // TMEM buffer whose stores are issued but not yet announced (tfull)
-    Stg<R> dvn[DD];  // DLDG: the next walker's direct operands, loaded one walker ahead
-    if constexpr (G::DLDG) {
-        if (my_tiles > 0) {
-            pdl_wait();  // the payloads may come from the previous kernel on the stream
-            ldg_direct<G>(P, 0, v3_tile<G>(P, v3_lin(0)), e0, lane, dvn);
-        }
-    }
     for (int k = 0; k < my_tiles; ++k) {
         const V3Tile t = v3_tile<G>(P, v3_lin(k));
         int ps = 0, pd = 0;
@@ -477,17 +448,8 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             const Cx<RG>* sh_u = reinterpret_cast<const Cx<RG>*>(smem_raw + (size_t)s * G::STAGE_BYTES + G::SH_OFF);
             const Cx<RG>* sh_d = sh_u + G::SH_ELEMS;
             Stg<R> dv[DD];
-            if constexpr (G::DLDG) {
 #pragma unroll
-                for (int d = 0; d < DD; ++d) dv[d] = dvn[d];
-                // the next walker's direct operands (this tile's or the next tile's first)
-                if (w + 1 < nb) ldg_direct<G>(P, w + 1, t, e0, lane, dvn);
-                else if (k + 1 < my_tiles) ldg_direct<G>(P, 0, v3_tile<G>(P, v3_lin(k + 1)), e0, lane, dvn);
-            } else {
-#pragma unroll
-                for (int d = 0; d < DD; ++d)
-                    dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
-            }
+            for (int d = 0; d < DD; ++d) dv[d] = widen<R>(lds_plain(dir_u + d * G::W + dr_o, dir_d + d * G::W + dr_o));
             constexpr int NJ = PP + DD - 1;  // diagonals p - d
             // The tile's last walker hands the block to TMEM as it completes: the
             // 8 entries of store c (planes 2c, 2c+1) are final after diagonal
@@ -672,7 +634,6 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
             G4_TRY(get_maps(staged[b0 + i], n, G::ES, G::NSH, G::W, G::DR, 2, &mp));
             tp.dmap[i] = mp.dmap;
             tp.smap[i] = mp.smap;
-            tp.stg[i] = staged[b0 + i];
         }
         tp.nx = (int32_t)((hi - lo + G::Q - 1) / G::Q);
         const int64_t tiles = (int64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
@@ -1012,16 +973,6 @@ g4_status launch_pst(int geom, bool exact, void* g4p, int64_t lo, int64_t hi, in
         case 42: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 3, 8>>(exact, g4p, lo, hi, n, staged, nbatch, st);
         case 43: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 3, 10>>(exact, g4p, lo, hi, n, staged, nbatch, st);
         case 44: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 2, 16>>(exact, g4p, lo, hi, n, staged, nbatch, st);
-        case 46:  // direct operands by LDG, 6 band-only stages (complex128 payloads only)
-            if constexpr (sizeof(RG) == 8)
-                return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 6, 4, true>>(exact, g4p, lo, hi, n, staged, nbatch,
-                                                                              st);
-            return launch_pst<RG>(40, exact, g4p, lo, hi, n, staged, nbatch, st);
-        case 47:  // ... 5 band-only stages, 8 park slots
-            if constexpr (sizeof(RG) == 8)
-                return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 5, 8, true>>(exact, g4p, lo, hi, n, staged, nbatch,
-                                                                              st);
-            return launch_pst<RG>(40, exact, g4p, lo, hi, n, staged, nbatch, st);
         default: return fail(G4_ERR_CONTRACT, "unknown v3 geometry");
     }
 }
@@ -1037,8 +988,6 @@ bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst) {
         case 43: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 3; return true;
         case 44: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 2; return true;
         case 45: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 7; return true;
-        case 46: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 6; return true;
-        case 47: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 5; return true;
         default: return false;
     }
 }

@@ -182,7 +182,6 @@ struct alignas(64) TmaParams {
     int32_t off;  // sheared-coordinate offset (elements), see make_maps
     int32_t hints;  // v3 lab knob (G4RING_V3_HINTS): 2 = L2 evict_last on the payload boxes
     long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
-    const void* stg[TMA_MAXW];  // the staged payloads (v3 geometries that read direct operands by LDG)
 };
 
 // Shared -> global bulk copy by the TMA engine: add (.add reduction) or store.
