@@ -274,6 +274,13 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + (size_t)NST * G::STAGE_BYTES);
     uint64_t* empty = full + NST;
 
+    // Programmatic dependent launch (non-cluster launches): the next K1 may be
+    // scheduled as this grid's last wave runs; every access to global memory
+    // (payload boxes, slice) waits for the previous kernel on the stream.
+    if constexpr (G::CL == 1) {
+        if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     constexpr int DR = G::DR, Q = G::Q;
@@ -698,8 +705,19 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
         const uint64_t ctas = (uint64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
         if (ctas >= (1ull << 31)) return fail(G4_ERR_CONTRACT, "accumulate: launch grid too large");
         if constexpr (G::CL == 1) {
-            k_accumulate_tma<R, RG, G, FUSED, MINB, EXP><<<(unsigned)ctas, G::THREADS, G::SMEM, st>>>(tp);
-            G4_TRY(check_cuda(cudaGetLastError(), "k_accumulate_tma launch"));
+            static const bool pdl = env_int("G4RING_PDL", 1) != 0;
+            cudaLaunchConfig_t lc = {};
+            lc.gridDim = dim3((unsigned)ctas);
+            lc.blockDim = dim3(G::THREADS);
+            lc.dynamicSmemBytes = G::SMEM;
+            lc.stream = st;
+            cudaLaunchAttribute at[1];
+            at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            at[0].val.programmaticStreamSerializationAllowed = 1;
+            lc.attrs = at;
+            lc.numAttrs = pdl ? 1 : 0;
+            G4_TRY(check_cuda(cudaLaunchKernelEx(&lc, k_accumulate_tma<R, RG, G, FUSED, MINB, EXP>, tp),
+                              "k_accumulate_tma launch"));
         } else {
             cudaLaunchConfig_t lc = {};
             lc.gridDim = dim3((unsigned)ctas);
