@@ -595,10 +595,11 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
 template <typename RG, class G, bool EXACT>
 static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, const void* const* staged,
                               int32_t nbatch, cudaStream_t st) {
-    // TMEM stores inside the last walker: -4 % at N = 1024 and -5 % at N = 4608,
-    // +5 % at N = 512 (lab r02n), so from N = 1024 on (G4RING_V3_EARLY_ST=0/1 forces)
+    // TMEM stores inside the last walker: -2 to -4 % at N = 1024 with 8 walkers,
+    // neutral to +5 % at N = 512, +7 to +10 % with 16 walkers (labs r02n, r02ab):
+    // from N = 1024 on, up to 8 walkers a pass (G4RING_V3_EARLY_ST=0/1 forces)
     static const int early_env = env_int("G4RING_V3_EARLY_ST", -1);
-    const bool early = early_env >= 0 ? early_env != 0 : n >= 1024;
+    const bool early = early_env >= 0 ? early_env != 0 : (n >= 1024 && std::min(nbatch, TMA_MAXW) <= 8);
     auto kern = early ? k_accumulate_pst<RG, G, true, EXACT> : k_accumulate_pst<RG, G, false, EXACT>;
     int dev = 0;
     G4_CUDA(cudaGetDevice(&dev));
