@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 const int pd = (G::ES == 8) ? (xd & 1) : 0, ps = (G::ES == 8) ? (xs & 1) : 0;
                 for (int w = 0; w < nb; ++w, ++it) {
                     const int s = it % NST;
-                    if (it >= NST) mbar_wait(&empty[s], ((it / NST) - 1) & 1);
+                    if (it >= NST) { if (P.hints & 64) mbar_wait_sleep(&empty[s], ((it / NST) - 1) & 1); else mbar_wait(&empty[s], ((it / NST) - 1) & 1); }
                     mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
                     unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
                     if (P.hints & 2) {
@@ -317,7 +317,8 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         for (int k = 0; k < drained; ++k) {
             const int b = k & 1;
             if (EXACT && k + 1 < drained) v3_prefetch_g4<G>(P, v3_tile<G>(P, v3_lin(k + 1)), q, lane);
-            mbar_wait(&tfull[b], (k >> 1) & 1);
+            if (P.hints & 64) mbar_wait_sleep(&tfull[b], (k >> 1) & 1);  // 64: suspend-time waits (lab)
+            else mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
             if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
             const V3Tile t = v3_tile<G>(P, v3_lin(k));

@@ -180,7 +180,8 @@ struct alignas(64) TmaParams {
     int32_t nbatch;
     int32_t nx;   // plane chunks
     int32_t off;  // sheared-coordinate offset (elements), see make_maps
-    int32_t hints;  // v3 lab knob (G4RING_V3_HINTS): 2 = L2 evict_last on the payload boxes
+    int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS): 2 = L2 evict_last on the payload boxes, 64 =
+                    // suspend-time waits for the producer and the epilogue (both within noise, r02ac)
     long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
 };
 
