@@ -827,7 +827,6 @@ static g4_status launch_v2_geom(int g, const AccParams<R, RG>& prm, cudaStream_t
         case 40:
         case 42:
         case 43:
-        case 48:
         case 44:  // v3, the persistent kernel (complex128 slices): fused + deferred, or exact
             if constexpr (sizeof(R) == 8)
                 return launch_pst<RG>(g, !FUSED, prm.g4, prm.lo, prm.hi, prm.n,
@@ -868,8 +867,7 @@ static bool geom_info(int g, GeomInfo* out) {
         case 42:
         case 43:
         case 44:
-        case 45:
-        case 48: {
+        case 45: {
             int pp, dd, q, dr, nst;
             pst_geom_info(g, &pp, &dd, &q, &dr, &nst);
             *out = {pp, dd, q, dr, nst, 1, 16};

@@ -46,12 +46,9 @@ namespace g4 {
 
 // Geometry: PP x DD thread block, CWQ x CWR consumer warps (CW = 8), NST
 // stages of both boxes, NPARK 2-KB park slots per epilogue warp.
-// PAIR: CTAs run as clusters of two on the tiles (2m, y, z) / (2m + 1, y, z);
-// those share the direct box, which rank 0 loads once for both by TMA multicast.
-template <typename RG, int PP_, int DD_, int CWQ_, int CWR_, int NST_, int NPARK_, bool PAIR_ = false>
+template <typename RG, int PP_, int DD_, int CWQ_, int CWR_, int NST_, int NPARK_>
 struct V3Geom {
     static constexpr int PP = PP_, DD = DD_, CWQ = CWQ_, CWR = CWR_, NST = NST_, NPARK = NPARK_;
-    static constexpr bool PAIR = PAIR_;
     static constexpr int CW = CWQ * CWR;
     static_assert(CW == 8, "two consumer warp groups");
     static constexpr int THREADS = 512;                      // 4 warp groups
@@ -220,29 +217,23 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     uint64_t* tfull = empty + NST;  // [2] consumers -> epilogue: the tile's blocks are in TMEM buffer b
     uint64_t* tready = tfull + 2;   // [2] epilogue -> consumers: TMEM buffer b has been drained
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tready + 2);
-    uint64_t* pair_done = tready + 3;  // PAIR, rank 0: rank 1's consumers are past their last remote arrive
 
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = P.nx * ((n + 31) / 32) * ((n + DR - 1) / DR);
-    // PAIR: cluster rank, and the pair's tiles 2 (pc + k npairs) + rank (nx even, grid even)
-    const int crank = G::PAIR ? (int)(blockIdx.x & 1) : 0;
-    const int npairs = (int)gridDim.x / 2, pc = (int)blockIdx.x / 2;
-    const int my_tiles = G::PAIR ? (pc < ntiles / 2 ? (ntiles / 2 - 1 - pc) / npairs + 1 : 0) : v3_count(ntiles);
-    auto tile_lin = [&](int k) { return G::PAIR ? 2 * (pc + k * npairs) + crank : v3_lin(k); };
+    const int my_tiles = v3_count(ntiles);
     const int nb = P.nbatch;
 
     if (threadIdx.x == 0) {
         trace_gt(P.trace, 0);
         for (int s = 0; s < NST; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], (G::PAIR && crank == 0) ? 2 * G::CW : G::CW);  // rank 0: both CTAs' consumers
+            mbar_init(&empty[s], G::CW);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull[b], G::CW);
             mbar_init(&tready[b], 4);
         }
-        if (G::PAIR && crank == 0) mbar_init(pair_done, G::CW);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         // the next K1 launch on this stream may start its prologue as our CTAs retire
         // (programmatic dependent launch; it waits for our completion before it reads
@@ -257,7 +248,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if constexpr (G::PAIR) cluster_sync_relaxed();  // both CTAs' barriers are initialised
     const uint32_t tmem = *tmem_slot;
 
     if (warp >= 12) {
@@ -268,7 +258,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 // Before waiting for the previous kernel: pull this CTA's first
                 // walkers' boxes into L2 (an L2 prefetch reads through the point of
                 // coherence, so it cannot yield stale data for the loads below)
-                const V3Tile t = v3_tile<G>(P, tile_lin(0));
+                const V3Tile t = v3_tile<G>(P, v3_lin(0));
                 const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
                 const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
                 const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
@@ -286,7 +276,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             const uint64_t keep = l2_policy_evict_last();  // payload rows are re-read by many tiles
             int it = 0;
             for (int k = 0; k < my_tiles; ++k) {
-                const V3Tile t = v3_tile<G>(P, tile_lin(k));
+                const V3Tile t = v3_tile<G>(P, v3_lin(k));
                 const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
                 const int C0 = wrap((int)(t.q0 - t.j0) - 31 - (DR - 1), n);
                 const int xd = t.j0 - t.k1_0 + P.off, xs = C0 - R0 + P.off;
@@ -296,13 +286,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                     if (it >= NST) { if (P.hints & 64) mbar_wait_sleep(&empty[s], ((it / NST) - 1) & 1); else mbar_wait(&empty[s], ((it / NST) - 1) & 1); }
                     mbar_arrive_expect_tx(&full[s], G::DIR_BYTES + G::SH_BYTES);
                     unsigned char* st = smem_raw + (size_t)s * G::STAGE_BYTES;
-                    if constexpr (G::PAIR) {
-                        // the direct box is the pair's: rank 0 writes it into both CTAs' stage s
-                        // (completion on each CTA's full[s]); each CTA loads its own band
-                        if (crank == 0)
-                            tma_load_3d_mc(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s], 3);
-                        tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
-                    } else if (P.hints & 2) {
+                    if (P.hints & 2) {
                         tma_load_3d_hint(st + G::DIR_OFF, &P.dmap[w], EW * (xd - pd), t.k1_0, 0, &full[s], keep);
                         tma_load_3d_hint(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s], keep);
                     } else {
@@ -312,9 +296,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 }
             }
             trace_gt(P.trace, 4);
-            // PAIR, rank 0: stay resident until rank 1's consumers made their last
-            // remote arrive on this CTA's barriers
-            if (G::PAIR && crank == 0) mbar_wait(pair_done, 0);
         }
         __syncwarp();
         return;
@@ -335,12 +316,12 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         const int drained = G::LAST_DIRECT ? my_tiles - 1 : my_tiles;  // see consumers
         for (int k = 0; k < drained; ++k) {
             const int b = k & 1;
-            if (EXACT && k + 1 < drained) v3_prefetch_g4<G>(P, v3_tile<G>(P, tile_lin(k + 1)), q, lane);
+            if (EXACT && k + 1 < drained) v3_prefetch_g4<G>(P, v3_tile<G>(P, v3_lin(k + 1)), q, lane);
             if (P.hints & 64) mbar_wait_sleep(&tfull[b], (k >> 1) & 1);  // 64: suspend-time waits (lab)
             else mbar_wait(&tfull[b], (k >> 1) & 1);
             tc_fence_after();
             if (P.trace && k < 31 && lane == 0) P.trace[((size_t)blockIdx.x * 32 + k) * 8 + 0 + 6 * (q == 3)] = clock64();
-            const V3Tile t = v3_tile<G>(P, tile_lin(k));
+            const V3Tile t = v3_tile<G>(P, v3_lin(k));
 #pragma unroll 1
             for (int h = 0; h < 2; ++h) {
                 const int cw = q + 4 * h, wq = cw % G::CWQ, wr = cw / G::CWQ;
@@ -420,7 +401,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
     int it = 0;
     int pend = -1;  // TMEM buffer whose stores are issued but not yet announced (tfull)
     for (int k = 0; k < my_tiles; ++k) {
-        const V3Tile t = v3_tile<G>(P, tile_lin(k));
+        const V3Tile t = v3_tile<G>(P, v3_lin(k));
         int ps = 0, pd = 0;
         if constexpr (G::ES == 8) {
             const int R0 = wrap((int)(t.q0 - t.k1_0) - (DR - 1), n);
@@ -512,10 +493,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             // an async-proxy write, the last ld.shared may still be in flight)
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
-            if (lane == 0) {
-                mbar_arrive(&empty[s]);
-                if (G::PAIR && crank == 1) mbar_arrive_remote(&empty[s], 0);  // rank 0 refills our DIR too
-            }
+            if (lane == 0) mbar_arrive(&empty[s]);
             if (pend >= 0) {  // the previous tile's TMEM stores, overlapped with this first walker
                 tmem_wait_st();
                 tc_fence_before();
@@ -613,7 +591,6 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             pend = -1;
         }
     }
-    if (G::PAIR && crank == 1 && lane == 0) mbar_arrive_remote(pair_done, 0);
 }
 
 template <typename RG, class G, bool EXACT>
@@ -663,11 +640,6 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         tp.nx = (int32_t)((hi - lo + G::Q - 1) / G::Q);
         const int64_t tiles = (int64_t)tp.nx * ((n + 31) / 32) * ((n + G::DR - 1) / G::DR);
         if (tiles >= (1ll << 31)) return fail(G4_ERR_CONTRACT, "accumulate: tile count too large");
-        if constexpr (G::PAIR) {  // the pair needs x pairs sharing (y, z): an even plane-chunk count
-            if ((tp.nx & 1) || tiles < 2)
-                return launch_pst_t<RG, V3Geom<RG, G::PP, G::DD, G::CWQ, G::CWR, G::NST, G::NPARK>, EXACT>(
-                    g4p, lo, hi, n, staged, nbatch, st);
-        }
         static const int grid_env = env_int("G4RING_V3_GRID", 0);  // lab: fewer CTAs than SMs
         const unsigned grid = (unsigned)std::min<int64_t>(tiles, grid_env > 0 ? std::min(grid_env, sms) : sms);
         static const char* trace_path = getenv("G4RING_V3_TRACE");  // lab: per-tile timeline dump
@@ -679,24 +651,15 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         }
         static const bool pdl = env_int("G4RING_PDL", 1) != 0;  // 0: no programmatic dependent launch (A/B)
         cudaLaunchConfig_t lc = {};
-        lc.gridDim = dim3(G::PAIR ? grid & ~1u : grid);
+        lc.gridDim = dim3(grid);
         lc.blockDim = dim3(G::THREADS);
         lc.dynamicSmemBytes = G::SMEM;
         lc.stream = st;
-        cudaLaunchAttribute attr[2];
-        int na = 0;
-        if (pdl) {
-            attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-            attr[na++].val.programmaticStreamSerializationAllowed = 1;
-        }
-        if (G::PAIR) {
-            attr[na].id = cudaLaunchAttributeClusterDimension;
-            attr[na].val.clusterDim.x = 2;
-            attr[na].val.clusterDim.y = 1;
-            attr[na++].val.clusterDim.z = 1;
-        }
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
         lc.attrs = attr;
-        lc.numAttrs = na;
+        lc.numAttrs = pdl ? 1 : 0;
         G4_TRY(check_cuda(cudaLaunchKernelEx(&lc, kern, tp), "k_accumulate_pst launch"));
         if (trace) {
             std::vector<long long> h((size_t)grid * 32 * 8);
@@ -1012,8 +975,6 @@ g4_status launch_pst(int geom, bool exact, void* g4p, int64_t lo, int64_t hi, in
         case 42: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 3, 8>>(exact, g4p, lo, hi, n, staged, nbatch, st);
         case 43: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 3, 10>>(exact, g4p, lo, hi, n, staged, nbatch, st);
         case 44: return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 2, 16>>(exact, g4p, lo, hi, n, staged, nbatch, st);
-        case 48:  // geometry 40 in CTA pairs sharing the direct box by TMA multicast
-            return launch_pst_mode<RG, V3Geom<RG, 8, 4, 2, 4, 4, 4, true>>(exact, g4p, lo, hi, n, staged, nbatch, st);
         default: return fail(G4_ERR_CONTRACT, "unknown v3 geometry");
     }
 }
@@ -1029,7 +990,6 @@ bool pst_geom_info(int geom, int* pp, int* dd, int* q, int* dr, int* nst) {
         case 43: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 3; return true;
         case 44: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 2; return true;
         case 45: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 7; return true;
-        case 48: *pp = 8, *dd = 4, *q = 16, *dr = 16, *nst = 4; return true;
         default: return false;
     }
 }
