@@ -41,6 +41,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <map>
 #include <tuple>
 
@@ -916,8 +917,34 @@ static bool use_v2(int n, int64_t planes) {
     return n >= 64 && (variant == 2 || (variant == 0 && planes >= 4));
 }
 
+// Chained fused passes (g4_k1.cuh): per stream, was the library's last K1
+// launch there a v3 fused pass?  dispatch_t rewrites the record after every
+// launch; launch_pst_t notes (per thread) that it launched such a pass.
+static std::mutex g_chain_mu;
+static std::unordered_map<cudaStream_t, bool> g_chain_prev;
+static thread_local bool t_chain_launched = false;
+
+bool k1_chain_prev(cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(g_chain_mu);
+    const auto it = g_chain_prev.find(st);
+    return it != g_chain_prev.end() && it->second;
+}
+void k1_chain_note(bool chain_safe) { t_chain_launched = chain_safe; }
+
+template <typename R, typename RG, bool FUSED>
+static g4_status dispatch_body(const AccParams<R, RG>& prm, cudaStream_t st);
+
 template <typename R, typename RG, bool FUSED>
 static g4_status dispatch_t(const AccParams<R, RG>& prm, cudaStream_t st) {
+    t_chain_launched = false;
+    const g4_status s = dispatch_body<R, RG, FUSED>(prm, st);
+    std::lock_guard<std::mutex> lk(g_chain_mu);
+    g_chain_prev[st] = s == G4_OK && t_chain_launched;
+    return s;
+}
+
+template <typename R, typename RG, bool FUSED>
+static g4_status dispatch_body(const AccParams<R, RG>& prm, cudaStream_t st) {
     const int64_t planes = prm.hi - prm.lo;
     if (use_v2(prm.n, planes))
         return launch_v2_geom<R, RG, FUSED>(

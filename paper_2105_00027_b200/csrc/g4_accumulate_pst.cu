@@ -235,9 +235,12 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             mbar_init(&tready[b], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        // the next K1 launch on this stream may start its prologue as our CTAs retire
-        // (programmatic dependent launch; it waits for our completion before it reads
-        // payloads or writes the slice)
+        // the next K1 launch on this stream may start as our CTAs retire (programmatic
+        // dependent launch; it waits for our completion before it reads payloads or
+        // writes the slice, unless it chains on us -- k1_chain_prev).  A fused pass
+        // that starts a chain lets the next launch begin only once its own
+        // predecessor is complete: chained passes do not wait for it.
+        if (!EXACT && !P.chain) pdl_wait();
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
     if (warp == 8) {  // the whole of TMEM (one CTA per SM)
@@ -272,7 +275,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                                  "r"(0) : "memory");
                 }
             }
-            pdl_wait();  // the payloads may come from the previous kernel on the stream
+            if (!P.chain) pdl_wait();  // the payloads may come from the previous kernel on the stream
             const uint64_t keep = l2_policy_evict_last();  // payload rows are re-read by many tiles
             int it = 0;
             for (int k = 0; k < my_tiles; ++k) {
@@ -296,6 +299,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
                 }
             }
             trace_gt(P.trace, 4);
+            if (P.chain) pdl_wait();  // chained: we complete only after the previous pass does
         }
         __syncwarp();
         return;
@@ -312,7 +316,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
         const uint64_t gmap = reinterpret_cast<uint64_t>(&P.gmap);
         int pair = 0;  // chunk pairs parked by this warp (slot = pair % NSLOT)
         constexpr int NSLOT = G::NPARK / 2;
-        pdl_wait();    // the previous kernel's slice updates land first
+        if (!P.chain) pdl_wait();  // the previous kernel's slice updates land first
         const int drained = G::LAST_DIRECT ? my_tiles - 1 : my_tiles;  // see consumers
         for (int k = 0; k < drained; ++k) {
             const int b = k & 1;
@@ -513,7 +517,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             const int k1b_d = t.k1_0 + e0;
             if (!(P.use_gmap && k1b_d + DD - 1 < n && t.j0 + 31 + e0 + DD - 1 < n)) {
                 // an edge block (row wrap / last column strip): every lane adds its own entries
-                pdl_wait();
+                if (!P.chain) pdl_wait();
                 const int np = min(PP, (int)(P.hi - P.lo) - p_lo_d);
 #pragma unroll
                 for (int p = 0; p < PP; ++p)
@@ -535,7 +539,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst(const __grid_constant
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             __syncwarp();
             if (lane == 0) {
-                pdl_wait();  // the previous kernel's slice updates land first
+                if (!P.chain) pdl_wait();  // the previous kernel's slice updates land first
                 // (an interior block: edge blocks took the per-lane path above)
                 const int np = min(PP, (int)(P.hi - P.lo) - p_lo_d);
                 for (int p = 0; p < np; ++p) {
@@ -630,6 +634,8 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         tp.use_gmap = g4_gmap_enabled() ? 1 : 0;
         static const int hints = env_int("G4RING_V3_HINTS", 0);  // A/B knob (lab)
         tp.hints = hints;
+        static const bool chain_on = env_int("G4RING_V3_CHAIN", 1) != 0;  // 0: every pass waits (A/B)
+        tp.chain = (!EXACT && chain_on && (b0 > 0 || k1_chain_prev(st))) ? 1 : 0;
         tp.nbatch = std::min(TMA_MAXW, nbatch - b0);
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
@@ -672,6 +678,7 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
             }
         }
     }
+    k1_chain_note(!EXACT);
     return G4_OK;
 }
 

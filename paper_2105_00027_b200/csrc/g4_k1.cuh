@@ -183,6 +183,9 @@ struct alignas(64) TmaParams {
     int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS): 2 = L2 evict_last on the payload boxes, 64 =
                     // suspend-time waits for the producer and the epilogue (both within noise, r02ac)
     long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
+    int32_t chain;     // v3 fused: the previous K1 on the stream was a v3 fused pass (slice
+                       // reductions only): no waits before the first loads and reductions, one
+                       // before the CTA exits (k1_chain_prev)
 };
 
 // Shared -> global bulk copy by the TMA engine: add (.add reduction) or store.
@@ -272,6 +275,17 @@ int sheared_offset(int n, int es);
 g4_status get_maps(const void* stg, int n, int es, int nsh, int width, int dd, int band_spins, MapPair* out);
 bool g4_gmap_enabled();
 g4_status slice_map(const void* g4, int n, int64_t planes, int pp, int dd, CUtensorMap* out);
+
+// Chained fused passes.  Two v3 fused passes on one stream touch the slice only
+// through reductions, which commute: the later one needs no griddepcontrol.wait
+// before its loads and reductions, only one before it exits (so its completion
+// still implies the earlier pass's).  The library records per stream whether
+// its last K1 launch there was such a pass (k1_chain_prev); any other K1 launch
+// clears the record, and a pass that starts a chain waits for its predecessor
+// before it lets the next launch begin.  Work of anything else between two
+// launches serialises the stream anyway (only K1 kernels trigger early).
+bool k1_chain_prev(cudaStream_t st);
+void k1_chain_note(bool chain_safe);
 
 // K1 v3 (g4_accumulate_pst.cu): the persistent fused update of a complex128
 // slice with payload entries RG; geometry ids 40-42.
