@@ -278,9 +278,17 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
     // Programmatic dependent launch (non-cluster launches): the next K1 may be
     // scheduled as this grid's last wave runs; every access to global memory
     // (payload boxes, slice) waits for the previous kernel on the stream.
+    // A deferred (reduce-only) pass chains like v3 (k1_chain_prev): chained, it
+    // does not wait here but before it exits; starting a chain, it waits before
+    // it lets the next launch begin.
     if constexpr (G::CL == 1) {
-        if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-        asm volatile("griddepcontrol.wait;" ::: "memory");
+        if constexpr ((EXP & K1_DEFER) != 0) {
+            if (!P.chain) asm volatile("griddepcontrol.wait;" ::: "memory");
+            if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+        } else {
+            if (threadIdx.x == 0) asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+        }
     }
     const int n = P.n;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -555,6 +563,9 @@ k_accumulate_tma(const __grid_constant__ TmaParams<R> P) {
                     }
                 }
     }
+    if constexpr ((EXP & K1_DEFER) != 0 && G::CL == 1) {  // chained: complete after the previous pass
+        if (P.chain && threadIdx.x == 0) asm volatile("griddepcontrol.wait;" ::: "memory");
+    }
 }
 
 // Host: the two sheared tensor maps of one staged payload, cached by (pointer, n, dtype).
@@ -694,6 +705,10 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
             tp.use_gmap = g4_gmap_enabled() ? 1 : 0;
         }
         tp.nbatch = std::min(TMA_MAXW, prm.nbatch - b0);
+        if constexpr ((EXP & K1_DEFER) != 0 && G::CL == 1) {
+            static const bool chain_on = env_int("G4RING_V3_CHAIN", 1) != 0;
+            tp.chain = (chain_on && (b0 > 0 || k1_chain_prev(st))) ? 1 : 0;
+        }
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
             G4_TRY(get_maps(prm.stg[b0 + i], n, G::ES, G::CL > 1 ? G::HS : G::NSH, G::W, G::DR,
@@ -736,6 +751,7 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
                               "k_accumulate_tma cluster launch"));
         }
     }
+    k1_chain_note((EXP & K1_DEFER) != 0 && G::CL == 1);
     return G4_OK;
 }
 

@@ -183,7 +183,7 @@ struct alignas(64) TmaParams {
     int32_t hints;  // v3 lab knobs (G4RING_V3_HINTS): 2 = L2 evict_last on the payload boxes, 64 =
                     // suspend-time waits for the producer and the epilogue (both within noise, r02ac)
     long long* trace;  // v3 lab timeline (G4RING_V3_TRACE), else null
-    int32_t chain;     // v3 fused: the previous K1 on the stream was a v3 fused pass (slice
+    int32_t chain;     // deferred passes: the previous K1 on the stream was one too (slice
                        // reductions only): no waits before the first loads and reductions, one
                        // before the CTA exits (k1_chain_prev)
 };
@@ -276,8 +276,8 @@ g4_status get_maps(const void* stg, int n, int es, int nsh, int width, int dd, i
 bool g4_gmap_enabled();
 g4_status slice_map(const void* g4, int n, int64_t planes, int pp, int dd, CUtensorMap* out);
 
-// Chained fused passes.  Two v3 fused passes on one stream touch the slice only
-// through reductions, which commute: the later one needs no griddepcontrol.wait
+// Chained fused passes.  Two deferred fused passes (v3, or v2 with K1_DEFER) on
+// one stream touch the slice only through reductions, which commute: the later one needs no griddepcontrol.wait
 // before its loads and reductions, only one before it exits (so its completion
 // still implies the earlier pass's).  The library records per stream whether
 // its last K1 launch there was such a pass (k1_chain_prev); any other K1 launch

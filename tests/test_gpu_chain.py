@@ -112,3 +112,36 @@ def test_chain_repeatable_many_passes(cuda_dev):
         _mode(lib, False)
     assert torch.equal(outs[0], outs[1])
     assert torch.equal(outs[0], one.data * 20)
+
+
+@pytest.mark.parametrize("case", ["p8_geom19", "c64_geom12", "b5_geom25", "v2_v3_alternating"])
+def test_chained_v2_deferred_passes(oracle, cuda_dev, case):
+    """The v2 deferred kernels chain too (and with v3): P = 8 (the 8-GPU ring
+    share), complex64 slices, 4-7 walkers a pass, and passes alternating
+    between 5 walkers (v2 geometry 25) and 8 (v3); integer payloads, bitwise."""
+    lib = _lib.load()
+    sp = T.CombinedIndexSpace(16, 32)
+    n = sp.size
+    planes, sizes, dt = {
+        "p8_geom19": (8, [8] * 6, torch.complex128),
+        "c64_geom12": (64, [8] * 5, torch.complex64),
+        "b5_geom25": (64, [5] * 5, torch.complex128),
+        "v2_v3_alternating": (64, [5, 8, 5, 8, 8, 5], torch.complex128),
+    }[case]
+    batches = [[T.generate_gsigma(60 + i, T.Origin(0, 0, w, 0, 0), sp, "integer", device=cuda_dev, dtype=dt)
+                for w in range(b)] for i, b in enumerate(sizes)]
+    sl = T.GtSlice.zeros(sp, 0, planes, device=cuda_dev, dtype=dt)
+    torch.cuda.synchronize()
+    _mode(lib, True)
+    try:
+        for gs in batches:
+            T.accumulate_g4_batch(sl, gs)
+        got = sl.data.cpu().numpy().astype(np.complex128)
+    finally:
+        _mode(lib, False)
+    ref = np.zeros((planes, n, n), np.complex128)
+    for gs in batches:
+        for g in gs:
+            oracle.accumulate(ref, 0, planes, g.up.contiguous().cpu().numpy().astype(np.complex128),
+                              g.down.contiguous().cpu().numpy().astype(np.complex128))
+    assert np.array_equal(got, ref)
