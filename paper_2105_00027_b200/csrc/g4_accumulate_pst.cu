@@ -744,6 +744,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst32(const __grid_consta
             mbar_init(&tready[b], 4);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        if (!P.chain) pdl_wait();  // chained passes as in the complex128 kernel (k1_chain_prev)
         asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     }
     if (warp == 8) {
@@ -760,7 +761,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst32(const __grid_consta
         // ---------------- producer (as the complex128 kernel) ----------------
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_PRODUCER) : "memory");
         if (threadIdx.x == 384) {
-            pdl_wait();
+            if (!P.chain) pdl_wait();
             int it = 0;
             for (int k = 0; k < my_tiles; ++k) {
                 const V3Tile t = v3_tile<G>(P, v3_lin(k));
@@ -777,6 +778,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst32(const __grid_consta
                     tma_load_3d(st + G::SH_OFF, &P.smap[w], EW * (xs - ps), R0, 0, &full[s]);
                 }
             }
+            if (P.chain) pdl_wait();  // chained: we complete only after the previous pass does
         }
         __syncwarp();
         return;
@@ -787,7 +789,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst32(const __grid_consta
         asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(V3_REG_EPILOGUE) : "memory");
         const int q = warp - 8;
         const uint32_t tq = tmem + ((uint32_t)(32 * q) << 16);
-        pdl_wait();
+        if (!P.chain) pdl_wait();
         for (int k = 0; k < my_tiles - 1; ++k) {  // the last tile: consumers
             const int b = k % NB;
             mbar_wait(&tfull[b], (k / NB) & 1);
@@ -874,7 +876,7 @@ __global__ void __launch_bounds__(512, 1) k_accumulate_pst32(const __grid_consta
             if (lane == 0) mbar_arrive(&empty[s]);
         }
         if (k == my_tiles - 1) {  // the last tile: straight from the registers
-            pdl_wait();
+            if (!P.chain) pdl_wait();
             const int p_lo = (int)(t.q0 - P.lo) + PP * wq;
             const int np = min(PP, (int)(P.hi - P.lo) - p_lo);
 #pragma unroll
@@ -934,6 +936,8 @@ static g4_status launch_pst32_t(void* g4p, int64_t lo, int64_t hi, int32_t n, co
         tp.n = n;
         tp.off = sheared_offset(n, G::ES);
         tp.nbatch = std::min(TMA_MAXW, nbatch - b0);
+        static const bool chain_on = env_int("G4RING_V3_CHAIN", 1) != 0;
+        tp.chain = (chain_on && (b0 > 0 || k1_chain_prev(st))) ? 1 : 0;
         for (int i = 0; i < tp.nbatch; ++i) {
             MapPair mp;
             G4_TRY(get_maps(staged[b0 + i], n, G::ES, G::NSH, G::W, G::DR, 2, &mp));
@@ -957,6 +961,7 @@ static g4_status launch_pst32_t(void* g4p, int64_t lo, int64_t hi, int32_t n, co
         lc.numAttrs = pdl ? 1 : 0;
         G4_TRY(check_cuda(cudaLaunchKernelEx(&lc, kern, tp), "k_accumulate_pst32 launch"));
     }
+    k1_chain_note(true);
     return G4_OK;
 }
 
