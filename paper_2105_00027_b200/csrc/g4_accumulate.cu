@@ -756,12 +756,14 @@ static g4_status launch_v2_t(const AccParams<R, RG>& prm, cudaStream_t st) {
 }
 
 // G4_ARITH_FUSED adds the walkers' sum to the slice at the end (K1_DEFER) with
-// >= 4 walkers per pass.  With the TMA bulk-reduce epilogue (complex128 slices)
+// >= 3 walkers per pass.  With the TMA bulk-reduce epilogue (complex128 slices)
 // this pays on any slice height: -2 % at P = 64, B = 8; -19 % at P = 8, B = 8
 // (the 8-GPU ring share); -7 % at N = 4608 (lab28).  With 1-2 walkers the L2
-// read-modify-write costs more than the G4 load it saves (+13 % / +5 %).
+// read-modify-write costs more than the G4 load it saves (+13 % / +5 %; with
+// chained passes +17 % / +6 %, lab r02al); at 3 walkers the chained deferred
+// pass wins (114.9 vs 125.2 us at the bench shape, lab r02al).
 static bool defer_update(int nbatch, int64_t planes) {
-    static const int min_w = env_int("G4RING_DEFER_MIN_WALKERS", 4);  // measurement knobs
+    static const int min_w = env_int("G4RING_DEFER_MIN_WALKERS", 3);  // measurement knobs
     static const int min_p = env_int("G4RING_DEFER_MIN_PLANES", 1);
     return nbatch >= min_w && planes >= min_p;
 }

@@ -389,7 +389,7 @@ def test_core_copy_plus_halo_rebuild_is_exact(cuda_dev, n, dtype):
                                               # complex64 kernel under G4RING_V3_C64=1)
                                               ("c64", 200, 0, 40, 9), ("c64", 128, 5, 37, 16)])
 def test_fused_deferred_update(oracle, cuda_dev, dtype, n, lo, hi, nb):
-    """G4_ARITH_FUSED with >= 4 walkers adds the walkers' sum to a NONZERO slice
+    """G4_ARITH_FUSED with >= 3 walkers adds the walkers' sum to a NONZERO slice
     at the end (L2 reduction): integer payloads stay bitwise, float within
     1e-12 (c128, mixed) / 1e-5 (c64) relative."""
     lib = _lib.load()
@@ -464,7 +464,7 @@ def test_cluster_multicast_geometry_parity():
     ("fused", "mixed", 16, 32, 64, 8, 40),
     ("fused", "c128", 48, 48, 16, 8, 43),    # N > 2048: v3 with 10 park slots
     ("fused", "c128", 16, 32, 64, 5, 25),    # 4-7 walkers: geometry 25
-    ("fused", "c128", 16, 32, 64, 2, 13),    # < 4 walkers: the exact kernel
+    ("fused", "c128", 16, 32, 64, 2, 13),    # < 3 walkers: the exact kernel
     ("exact", "c128", 16, 32, 64, 8, 13),
     ("fused", "c64", 16, 32, 64, 8, 12),
     ("fused", "c128", 16, 32, 8, 8, 19),     # the 8-GPU share of config 2
