@@ -632,8 +632,12 @@ static g4_status launch_pst_t(void* g4p, int64_t lo, int64_t hi, int32_t n, cons
         tp.off = sheared_offset(n, G::ES);
         G4_TRY(slice_map(g4p, n, hi - lo, 1, G::DD, &tp.gmap));
         tp.use_gmap = g4_gmap_enabled() ? 1 : 0;
-        static const int hints = env_int("G4RING_V3_HINTS", 0);  // A/B knob (lab)
-        tp.hints = hints;
+        // Payload boxes with an L2 evict_last policy up to N = 2048, where the
+        // walkers' payloads fit L2 next to the streaming slice: -1.2 % at the
+        // bench shape over five alternations, neutral at N = 1024 and P = 32
+        // (lab r02ao).  G4RING_V3_HINTS overrides (lab knobs, TmaParams::hints).
+        static const int hints_env = env_int("G4RING_V3_HINTS", -1);
+        tp.hints = hints_env >= 0 ? hints_env : (n <= 2048 ? 2 : 0);
         static const bool chain_on = env_int("G4RING_V3_CHAIN", 1) != 0;  // 0: every pass waits (A/B)
         tp.chain = (!EXACT && chain_on && (b0 > 0 || k1_chain_prev(st))) ? 1 : 0;
         tp.nbatch = std::min(TMA_MAXW, nbatch - b0);
